@@ -1,0 +1,60 @@
+"""Single-kernel entry points over the C ABI (vpe_op_*), used by parity tests and microbenchmarks."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import check, lib
+
+EPI_BF16, EPI_RESID, EPI_F32 = 0, 1, 3
+ACT_NONE, ACT_GELU, ACT_RELU = 0, 1, 2
+
+
+def _s(stream):
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream if stream is None else stream)
+
+
+def _p(t):
+    return C.c_void_p(None if t is None else t.data_ptr())
+
+
+def linear(a: torch.Tensor, w: torch.Tensor, bias=None, scale=None, out=None, kind=EPI_BF16, act=ACT_NONE,
+           bn=64, k_in=None, stream=None) -> torch.Tensor:
+    """a: bf16 [M,K]; w: bf16 [N,Kw] (Kw multiple of K); returns bf16/f32 [M,N] (or updates out)."""
+    M, K = a.shape
+    N, Kw = w.shape
+    if out is None:
+        out = torch.empty(M, N, device=a.device, dtype=torch.bfloat16 if kind == EPI_BF16 else torch.float32)
+    check(lib.vpe_op_linear(_p(a), M, K, _p(w), N, Kw, _p(bias), _p(scale), _p(out), kind, act, bn, _s(stream)),
+          "vpe_op_linear")
+    return out
+
+
+def conv(x: torch.Tensor, w: torch.Tensor, C_real: int, ks: int, bias=None, add1=None, add2=None, act=ACT_NONE,
+         out=None, out_relu=None, ldo=None, stream=None):
+    """x: bf16 NHWC [B,H,W,Cp]; w: bf16 [N, ks*ks*Cp]."""
+    B, H, W, Cp = x.shape
+    N = w.shape[0]
+    ldo = ldo or N
+    if out is None:
+        out = torch.zeros(B, H, W, ldo, device=x.device, dtype=torch.bfloat16)
+    check(lib.vpe_op_conv(_p(x), B, H, W, C_real, Cp, ks, _p(w), N, _p(bias), _p(add1), _p(add2), _p(out),
+                          _p(out_relu), ldo, act, _s(stream)), "vpe_op_conv")
+    return out
+
+
+def attention(qkv: torch.Tensor, B: int, T: int, D: int, heads: int, stream=None) -> torch.Tensor:
+    out = torch.empty(B * T, D, device=qkv.device, dtype=torch.bfloat16)
+    check(lib.vpe_op_attention(_p(qkv), _p(out), B, T, D, heads, _s(stream)), "vpe_op_attention")
+    return out
+
+
+def layernorm(x: torch.Tensor, w, b, eps=1e-6, w2=None, b2=None, stream=None):
+    M, D = x.shape
+    out = torch.empty(M, D, device=x.device, dtype=torch.bfloat16)
+    out2 = torch.empty_like(out) if w2 is not None else None
+    check(lib.vpe_op_layernorm(_p(x), M, D, _p(w), _p(b), eps, _p(out), _p(w2), _p(b2), _p(out2), _s(stream)),
+          "vpe_op_layernorm")
+    return out if out2 is None else (out, out2)

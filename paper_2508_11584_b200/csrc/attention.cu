@@ -1,0 +1,252 @@
+// Non-causal multi-head attention (head_dim 64) on tcgen05: S = Q K^T and O_j = P_j V_j run on
+// the tensor cores with both accumulators in TMEM; softmax runs on 4 warps, one thread per
+// query row, with the online max/sum rescale applied in registers.
+//
+// Oracle: transformers modeling_dinov2.py:153-178 (eager softmax(QK^T * 1/8) V).
+// Q/K/V are read in place from the fused QKV GEMM output [B*T, 3D] through a 2D TMA map
+// (box 64 cols x 128 rows), so no head re-layout pass is needed.
+#include <cudaTypedefs.h>
+
+#include "attention.cuh"
+#include "tc.cuh"
+#include "util.cuh"
+
+namespace vpe {
+
+namespace {
+constexpr int TILE = 16 * 1024;  // one [128][64] bf16 SW128 tile
+constexpr int SMEM_ATT = 1024 + TILE /*Q*/ + 2 * TILE /*K*/ + 2 * TILE /*V*/ + 2 * TILE /*P*/ + 256;
+constexpr int S_COL = 0, O_COL = 128, TMEM_COLS = 256;
+}  // namespace
+
+__global__ void __launch_bounds__(192, 1)
+    attention_tc_kernel(const __grid_constant__ CUtensorMap tqkv, __nv_bfloat16* __restrict__ out, int T, int D,
+                        float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + TILE;
+  uint8_t* sV = sK + 2 * TILE;
+  uint8_t* sP = sV + 2 * TILE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * TILE);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;   // [2]
+  uint64_t* v_full = bars + 3;   // [2]
+  uint64_t* kv_empty = bars + 5; // [2]
+  uint64_t* s_full = bars + 7;
+  uint64_t* p_full = bars + 8;
+  uint64_t* o_full = bars + 9;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
+
+  const int qt = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
+  const int q0 = qt * 128;
+  const int row_base = b * T;
+  const int nkv = (T + 127) / 128;
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tqkv);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128);
+    mbar_init(o_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, TILE);
+      tma_load_2d(sQ, &tqkv, q_full, head * 64, row_base + q0);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j & 1;
+        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[s], TILE);
+        tma_load_2d(sK + s * TILE, &tqkv, &k_full[s], D + head * 64, row_base + j * 128);
+        mbar_expect_tx(&v_full[s], TILE);
+        tma_load_2d(sV + s * TILE, &tqkv, &v_full[s], 2 * D + head * 64, row_base + j * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16(128, 128);
+      constexpr uint32_t idesc_o = idesc_bf16(128, 64, /*b_mn_major=*/true);
+      const uint32_t q_addr = smem_u32(sQ);
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      {
+        const uint32_t k_addr = smem_u32(sK);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_f16(tmem + S_COL, smem_desc(q_addr + k * 32, 16, 1024, 2), smem_desc(k_addr + k * 32, 16, 1024, 2),
+                   idesc_s, k > 0);
+        umma_commit(s_full);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+        if (j + 1 < nkv) {
+          const int s1 = (j + 1) & 1;
+          mbar_wait(&k_full[s1], ((j + 1) >> 1) & 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(sK + s1 * TILE);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_f16(tmem + S_COL, smem_desc(q_addr + k * 32, 16, 1024, 2), smem_desc(k_addr + k * 32, 16, 1024, 2),
+                     idesc_s, k > 0);
+          umma_commit(s_full);
+        }
+        const int s = j & 1;
+        mbar_wait(&v_full[s], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sV + s * TILE);
+        const uint32_t p_addr = smem_u32(sP);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t pa = p_addr + (k >> 2) * TILE + (k & 3) * 32;
+          umma_f16(tmem + O_COL, smem_desc(pa, 16, 1024, 2), smem_desc(v_addr + k * 2048, 1024, 1024, 2), idesc_o,
+                   k > 0);
+        }
+        umma_commit(o_full);
+        umma_commit(&kv_empty[s]);
+      }
+    }
+  } else {
+    // softmax / correction warps: one thread per query row
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
+    float m_prev = -INFINITY, l = 0.f, alpha_prev = 1.f;
+    float o_acc[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) o_acc[i] = 0.f;
+    uint8_t* prow0 = sP + r * 128;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      const int kvalid = T - j * 128;  // keys >= kvalid are padding
+      float sv[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float t[32];
+        tmem_ld32(lane_addr + S_COL + c * 32, t);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = (c * 32 + i < kvalid) ? t[i] * scale_log2 : -INFINITY;
+      }
+      float mx = m_prev;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) mx = fmaxf(mx, sv[i]);
+      const float alpha = exp2f(m_prev - mx);  // m_prev=-inf on first block -> 0
+      float rs = 0.f;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        sv[i] = exp2f(sv[i] - mx);
+        rs += sv[i];
+      }
+      l = l * alpha + rs;
+      m_prev = mx;
+      // O_{j-1} must be consumed (and PV_{j-1} finished reading P) before P_j is written
+      if (j > 0) {
+        mbar_wait(o_full, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float t[32];
+          tmem_ld32(lane_addr + O_COL + c * 32, t);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o_acc[c * 32 + i] = o_acc[c * 32 + i] * alpha_prev + t[i];
+        }
+      }
+      alpha_prev = alpha;
+      // write P_j (bf16) in the UMMA SW128 K-major layout: two [128][64] tiles
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        uint8_t* prow = prow0 + t * TILE;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float* x = sv + t * 64 + c * 8;
+          uint4 u;
+          u.x = pack_bf16(x[0], x[1]);
+          u.y = pack_bf16(x[2], x[3]);
+          u.z = pack_bf16(x[4], x[5]);
+          u.w = pack_bf16(x[6], x[7]);
+          *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = u;
+        }
+      }
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    mbar_wait(o_full, (nkv - 1) & 1);
+    tc_fence_after();
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float t[32];
+      tmem_ld32(lane_addr + O_COL + c * 32, t);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o_acc[c * 32 + i] = o_acc[c * 32 + i] * alpha_prev + t[i];
+    }
+    const int qi = q0 + r;
+    if (qi < T) {
+      const float inv = 1.f / l;
+      uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(row_base + qi) * D + head * 64);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint4 u;
+        u.x = pack_bf16(o_acc[8 * c + 0] * inv, o_acc[8 * c + 1] * inv);
+        u.y = pack_bf16(o_acc[8 * c + 2] * inv, o_acc[8 * c + 3] * inv);
+        u.z = pack_bf16(o_acc[8 * c + 4] * inv, o_acc[8 * c + 5] * inv);
+        u.w = pack_bf16(o_acc[8 * c + 6] * inv, o_acc[8 * c + 7] * inv);
+        dst[c] = u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, int B, int T, int D, int heads) {
+  if (D != heads * 64) return VPE_E_SHAPE;
+  uint64_t dims[2] = {(uint64_t)(3 * D), (uint64_t)B * T};
+  uint64_t strides[1] = {(uint64_t)3 * D * 2};
+  uint32_t box[2] = {64u, 128u};
+  int rc = encode_tma(&a->tqkv, 2, qkv, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
+  a->out = out;
+  a->B = B;
+  a->T = T;
+  a->D = D;
+  a->heads = heads;
+  return VPE_OK;
+}
+
+int launch_attention(const AttnPlan& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
+    attr = true;
+  }
+  dim3 grid((a.T + 127) / 128, a.heads, a.B);
+  const float scale_log2 = 0.125f * 1.4426950408889634f;
+  attention_tc_kernel<<<grid, 192, SMEM_ATT, s>>>(a.tqkv, a.out, a.T, a.D, scale_log2);
+  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+}
+
+}  // namespace vpe

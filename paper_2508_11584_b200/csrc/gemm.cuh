@@ -1,0 +1,88 @@
+// tcgen05/TMEM/TMA GEMM engine for sm_100a: D[M,N] = A[M,K] * B[N,K]^T with fused epilogues.
+//
+// A is either a row-major activation matrix (mode ROWS) or an NHWC bf16 image read as an
+// implicit-GEMM convolution (mode CONV, kernel 1x1 or 3x3, stride 1, zero padding supplied by
+// TMA out-of-bounds fill). B is a K-major bf16 weight matrix. One CTA computes a 128 x BN tile:
+// warp 0 issues TMA, warp 1 issues tcgen05.mma (accumulator in TMEM), warps 2-5 run the epilogue.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace vpe {
+
+enum EpiKind : int {
+  EPI_BF16 = 0,   // out_bf16 = act(acc + bias)            [+ optional relu copy]
+  EPI_RESID = 1,  // resid_f32 += scale * (acc + bias)     (LayerScale + residual)
+  EPI_PATCH = 2,  // resid_f32[row remapped past cls] = acc + bias + pos
+  EPI_F32 = 3,    // out_f32 = acc + bias
+  EPI_CONV = 4,   // out_bf16 = act(acc + bias + add1 + add2) [+ relu copy]  (NHWC)
+  EPI_CONVT = 5,  // ConvTranspose(k=s) scatter into NHWC: col = (ky*k+kx)*cout + co
+  EPI_DEPTH = 6,  // depth = relu(b3 + sum_c relu(acc_c + bias_c) * w3_c) * max_depth
+};
+enum Act : int { ACT_NONE = 0, ACT_GELU = 1, ACT_RELU = 2 };
+
+struct EpiParams {
+  int kind = EPI_BF16;
+  int act = ACT_NONE;
+  int N = 0;                       // valid output columns
+  const float* bias = nullptr;     // [N]
+  const float* scale = nullptr;    // [N] (EPI_RESID)
+  void* out = nullptr;             // bf16 / f32 output
+  int64_t ldo = 0;                 // output row (pixel) pitch, elements
+  __nv_bfloat16* out_relu = nullptr;  // optional relu(out) copy, same pitch as out
+  float* resid = nullptr;          // fp32 residual stream
+  int64_t ldr = 0;
+  const __nv_bfloat16* add1 = nullptr;  // NHWC adds (pitch ldo)
+  const __nv_bfloat16* add2 = nullptr;
+  const float* pos = nullptr;      // EPI_PATCH: [T, N] position embedding
+  int rows_per_img = 0;            // EPI_PATCH: Np
+  int ct_k = 0, ct_cout = 0;       // EPI_CONVT: factor, real out channels
+  int ct_H = 0, ct_W = 0;          // EPI_CONVT: input grid (output grid = k*H x k*W)
+  const float* w3 = nullptr;       // EPI_DEPTH: [32]
+  float b3 = 0.f, max_depth = 1.f;
+  float* depth_pre = nullptr;      // EPI_DEPTH outputs [pixels]
+  float* depth = nullptr;
+};
+
+struct GemmParams {
+  int kblocks = 0;     // K blocks on the B side
+  int kblocks_a = 0;   // A-side K blocks before wrap-around (split-precision weights repeat A)
+  int mode = 0;        // 0 rows, 1 conv
+  int M = 0;           // mode 0: valid rows
+  int ks = 1;          // conv kernel size
+  int cchunks = 1;     // channel chunks (of BK) per tap
+  int H = 0, W = 0, bw = 0, bh = 0, tiles_x = 0, tiles_per_img = 0;
+  EpiParams ep;
+};
+
+struct GemmPlan {
+  CUtensorMap ta;
+  CUtensorMap tb;
+  GemmParams p;
+  dim3 grid;
+  int bn = 0, bk = 0;
+  size_t smem = 0;
+};
+
+// --- host-side builders (gemm.cu) ---
+bool tma_available();
+// Row-major A [M, K] (pitch lda elements) times K-major weights B [N, Kb] (pitch ldb).
+// Kb may be a multiple of K (split-precision weights concatenated along K; A repeats).
+int plan_gemm_rows(GemmPlan* g, const __nv_bfloat16* A, int M, int K, int64_t lda,
+                   const __nv_bfloat16* B, int N, int Kb, int64_t ldb, const EpiParams& ep, int bn);
+// NHWC image X (channels C real, pitches in elements: pixel, row, image) as implicit-GEMM conv
+// input; weights B [N, Kb] with Kb = ks*ks*Cpad (+ repeats), tap-major then channel.
+int plan_gemm_conv(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, int C,
+                   int64_t pitch_px, int64_t pitch_row, int64_t pitch_img, int ks, int bk,
+                   const __nv_bfloat16* B, int N, int Kb, int64_t ldb, const EpiParams& ep, int bn);
+int launch_gemm(const GemmPlan& g, cudaStream_t stream);
+
+}  // namespace vpe
+
+namespace vpe {
+// cuTensorMapEncodeTiled wrapper (bf16, zero OOB fill); dims/strides innermost first.
+int encode_tma(CUtensorMap* m, int rank, const void* ptr, const uint64_t* dims, const uint64_t* strides_bytes,
+               const uint32_t* box, CUtensorMapSwizzle swz);
+}  // namespace vpe

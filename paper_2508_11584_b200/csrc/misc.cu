@@ -1,0 +1,205 @@
+// Memory-bound kernels of the backbone and DPT neck: patch im2col + normalisation, LayerNorm
+// (optionally writing the tap LayerNorm straight into a ring slot), bilinear resize, stride-2
+// im2col. All coalesced, 16-byte vectorised, one pass over HBM/L2.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "misc.cuh"
+#include "tc.cuh"
+#include "util.cuh"
+
+namespace vpe {
+
+// ---------------------------------------------------------------------------------------------
+// u8 NCHW frames -> normalised bf16 im2col rows [B*Np, KP] (k = c*196 + ky*14 + kx, zero pad to KP)
+// Oracle: torchvision-style ImageNet normalisation + modeling_dinov2.py:139-149.
+// Also writes the cls rows of the fp32 residual stream: h[b*T] = cls_token + pos[0].
+__global__ void patch_im2col_kernel(const uint8_t* __restrict__ px, __nv_bfloat16* __restrict__ A, int B, int R,
+                                    int KP, float* __restrict__ resid, const float* __restrict__ cls_pos0, int D) {
+  const int h = R / 14, np = h * h;
+  const int blk = blockIdx.x;
+  if (blk >= B * np) {
+    const int b = blk - B * np;
+    float* dst = resid + (int64_t)b * (np + 1) * D;
+    for (int i = threadIdx.x; i < D; i += blockDim.x) dst[i] = cls_pos0[i];
+    return;
+  }
+  const int b = blk / np, p = blk - b * np;
+  const int py = p / h, pxx = p - py * h;
+  const float mean[3] = {0.485f, 0.456f, 0.406f};
+  const float stdv[3] = {0.229f, 0.224f, 0.225f};
+  __nv_bfloat16* row = A + (int64_t)blk * KP;
+  for (int k = threadIdx.x; k < KP; k += blockDim.x) {
+    float v = 0.f;
+    if (k < 588) {
+      const int c = k / 196, r = k - c * 196, ky = r / 14, kx = r - ky * 14;
+      const uint8_t u = px[(((int64_t)b * 3 + c) * R + (py * 14 + ky)) * R + pxx * 14 + kx];
+      v = ((float)u / 255.0f - mean[c]) / stdv[c];
+    }
+    row[k] = __float2bfloat16_rn(v);
+  }
+}
+
+int launch_patch_im2col(const uint8_t* px, __nv_bfloat16* A, int B, int R, int KP, float* resid,
+                        const float* cls_pos0, int D, cudaStream_t s) {
+  const int np = (R / 14) * (R / 14);
+  patch_im2col_kernel<<<B * np + B, 128, 0, s>>>(px, A, B, R, KP, resid, cls_pos0, D);
+  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------------------------
+// LayerNorm over D (multiple of 128) for fp32 rows -> bf16; optional second affine (tap LN).
+// Two-pass mean/variance in registers (matches torch's reduction numerics closely).
+template <int NV>
+__global__ void layernorm_kernel(const float* __restrict__ x, int M, int D, const float* __restrict__ w,
+                                 const float* __restrict__ b, float eps, __nv_bfloat16* __restrict__ out,
+                                 const float* __restrict__ w2, const float* __restrict__ b2,
+                                 __nv_bfloat16* __restrict__ out2) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)row * D);
+  float4 v[NV];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    v[i] = xr[i * 32 + lane];
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float a = v[i].x - mean, bb = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
+    q += (a * a + bb * bb) + (c * c + d * d);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / D + eps);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * 4;
+    const float n0 = (v[i].x - mean) * rstd, n1 = (v[i].y - mean) * rstd;
+    const float n2 = (v[i].z - mean) * rstd, n3 = (v[i].w - mean) * rstd;
+    if (out) {
+      const float4 ww = __ldg(reinterpret_cast<const float4*>(w + c));
+      const float4 bb = __ldg(reinterpret_cast<const float4*>(b + c));
+      uint2 u;
+      u.x = pack_bf16(n0 * ww.x + bb.x, n1 * ww.y + bb.y);
+      u.y = pack_bf16(n2 * ww.z + bb.z, n3 * ww.w + bb.w);
+      *reinterpret_cast<uint2*>(out + (int64_t)row * D + c) = u;
+    }
+    if (out2) {
+      const float4 ww = __ldg(reinterpret_cast<const float4*>(w2 + c));
+      const float4 bb = __ldg(reinterpret_cast<const float4*>(b2 + c));
+      uint2 u;
+      u.x = pack_bf16(n0 * ww.x + bb.x, n1 * ww.y + bb.y);
+      u.y = pack_bf16(n2 * ww.z + bb.z, n3 * ww.w + bb.w);
+      *reinterpret_cast<uint2*>(out2 + (int64_t)row * D + c) = u;
+    }
+  }
+}
+
+int launch_layernorm(const float* x, int M, int D, const float* w, const float* b, float eps, __nv_bfloat16* out,
+                     const float* w2, const float* b2, __nv_bfloat16* out2, cudaStream_t s) {
+  if (D % 128) return VPE_E_SHAPE;
+  const int rows_per_block = 8;
+  dim3 grid((M + rows_per_block - 1) / rows_per_block), block(32 * rows_per_block);
+  switch (D / 128) {
+#define VPE_LN(NV_) \
+  case NV_: layernorm_kernel<NV_><<<grid, block, 0, s>>>(x, M, D, w, b, eps, out, w2, b2, out2); break;
+    VPE_LN(1) VPE_LN(2) VPE_LN(3) VPE_LN(4) VPE_LN(5) VPE_LN(6) VPE_LN(8) VPE_LN(10) VPE_LN(12)
+#undef VPE_LN
+    default:
+      return VPE_E_SHAPE;
+  }
+  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Bilinear resize on NHWC bf16, align_corners=True (modeling_depth_anything.py:157-200, 288-293).
+// Thread = 8 channels of one output pixel. Input/output channel pitch cp (elements), C real.
+__global__ void bilinear_ac_kernel(const __nv_bfloat16* __restrict__ in, int B, int Hi, int Wi, int cp,
+                                   __nv_bfloat16* __restrict__ out, int Ho, int Wo, int C) {
+  const int cv = C / 8;
+  const int64_t total = (int64_t)B * Ho * Wo * cv;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const int c8 = (int)(t % cv);
+  int64_t pix = t / cv;
+  const int ox = (int)(pix % Wo);
+  pix /= Wo;
+  const int oy = (int)(pix % Ho);
+  const int b = (int)(pix / Ho);
+  const float sh = Ho > 1 ? (float)(Hi - 1) / (float)(Ho - 1) : 0.f;
+  const float sw = Wo > 1 ? (float)(Wi - 1) / (float)(Wo - 1) : 0.f;
+  const float fy = sh * oy, fx = sw * ox;
+  const int y0 = (int)fy, x0 = (int)fx;
+  const int y1 = y0 + (y0 < Hi - 1), x1 = x0 + (x0 < Wi - 1);
+  const float ly = fy - y0, lx = fx - x0;
+  const float hy = 1.f - ly, hx = 1.f - lx;
+  const __nv_bfloat16* base = in + (int64_t)b * Hi * Wi * cp + c8 * 8;
+  const uint4 a = *reinterpret_cast<const uint4*>(base + ((int64_t)y0 * Wi + x0) * cp);
+  const uint4 bq = *reinterpret_cast<const uint4*>(base + ((int64_t)y0 * Wi + x1) * cp);
+  const uint4 c = *reinterpret_cast<const uint4*>(base + ((int64_t)y1 * Wi + x0) * cp);
+  const uint4 d = *reinterpret_cast<const uint4*>(base + ((int64_t)y1 * Wi + x1) * cp);
+  const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&bq);
+  const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
+  const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d);
+  uint4 o;
+  uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 fa = __bfloat1622float2(pa[j]), fb = __bfloat1622float2(pb[j]);
+    const float2 fc = __bfloat1622float2(pc[j]), fd = __bfloat1622float2(pd[j]);
+    const float r0 = hy * (hx * fa.x + lx * fb.x) + ly * (hx * fc.x + lx * fd.x);
+    const float r1 = hy * (hx * fa.y + lx * fb.y) + ly * (hx * fc.y + lx * fd.y);
+    po[j] = pack_bf16(r0, r1);
+  }
+  *reinterpret_cast<uint4*>(out + (((int64_t)b * Ho + oy) * Wo + ox) * cp + c8 * 8) = o;
+}
+
+int launch_bilinear_ac(const __nv_bfloat16* in, int B, int Hi, int Wi, int cp, __nv_bfloat16* out, int Ho, int Wo,
+                       int C, cudaStream_t s) {
+  if (C % 8 || cp % 8) return VPE_E_SHAPE;
+  const int64_t total = (int64_t)B * Ho * Wo * (C / 8);
+  bilinear_ac_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(in, B, Hi, Wi, cp, out, Ho, Wo, C);
+  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------------------------
+// im2col for a 3x3 stride-2 pad-1 conv on NHWC bf16 [B,H,W,C] -> [B*Ho*Wo, 9*C] (tap-major)
+__global__ void im2col_s2_kernel(const __nv_bfloat16* __restrict__ x, int B, int H, int W, int C,
+                                 __nv_bfloat16* __restrict__ out, int Ho, int Wo) {
+  const int cv = C / 8;
+  const int64_t total = (int64_t)B * Ho * Wo * 9 * cv;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const int c8 = (int)(t % cv);
+  int64_t r = t / cv;
+  const int tap = (int)(r % 9);
+  r /= 9;
+  const int ox = (int)(r % Wo);
+  r /= Wo;
+  const int oy = (int)(r % Ho);
+  const int b = (int)(r / Ho);
+  const int iy = 2 * oy - 1 + tap / 3, ix = 2 * ox - 1 + tap % 3;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (iy >= 0 && iy < H && ix >= 0 && ix < W)
+    v = *reinterpret_cast<const uint4*>(x + (((int64_t)b * H + iy) * W + ix) * C + c8 * 8);
+  *reinterpret_cast<uint4*>(out + ((((int64_t)b * Ho + oy) * Wo + ox) * 9 + tap) * C + c8 * 8) = v;
+}
+
+int launch_im2col_s2(const __nv_bfloat16* x, int B, int H, int W, int C, __nv_bfloat16* out, cudaStream_t s) {
+  if (C % 8) return VPE_E_SHAPE;
+  const int Ho = (H + 1) / 2, Wo = (W + 1) / 2;
+  const int64_t total = (int64_t)B * Ho * Wo * 9 * (C / 8);
+  im2col_s2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(x, B, H, W, C, out, Ho, Wo);
+  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+}
+
+}  // namespace vpe

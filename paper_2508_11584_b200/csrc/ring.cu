@@ -1,0 +1,583 @@
+// Device feature ring: the reference's LATEST/FIFO channel state machine
+// (fanpipe/channels.py:1-594) over an HBM (or pinned-host) slot arena, with CUDA-event
+// producer/consumer handoff instead of bytes-visible-on-store.
+//
+// The control block keeps the reference's PECH1 header layout byte for byte
+// (channels.py:14-26): magic, mode u8 @6, capacity u32 @8, slot records stride 24 from 16
+// {state u32, frame_id u64 @8, capture_ts u64 @16}, 16 cursor entries stride 16
+// {consumer_id u32, last_frame u64 @8}, then producer_drops, evictions, pushed, consumed (u64).
+// State words use the reference's acquire/release CAS protocol (_kernels.pyx:18-37).
+//
+// GPU meaning of the states: READY = the producer's writes are *enqueued* and the slot's ready
+// event is recorded on the producer stream; every lease makes the consumer stream wait on that
+// event (RAW). A consumer's commit records its done event; a producer re-claiming the slot makes
+// its stream wait on every consumer's last done event for that slot (WAR). So host-side lease
+// counting orders the host, events order the device.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <thread>
+
+#include "util.cuh"
+
+namespace {
+
+constexpr uint32_t STATE_FREE = 0, STATE_WRITING = 1, STATE_READY = 2;
+constexpr int SLOT0 = 16, SLOT_STRIDE = 24, CURSOR_STRIDE = 16;
+constexpr int ALIGN = 64, ARENA_HDR = 64;
+std::atomic<int64_t> g_copies{0};
+
+inline uint32_t ld32(const void* p) { return __atomic_load_n(static_cast<const uint32_t*>(p), __ATOMIC_ACQUIRE); }
+inline void st32(void* p, uint32_t v) { __atomic_store_n(static_cast<uint32_t*>(p), v, __ATOMIC_RELEASE); }
+inline uint32_t cas32(void* p, uint32_t expected, uint32_t desired) {
+  __atomic_compare_exchange_n(static_cast<uint32_t*>(p), &expected, desired, false, __ATOMIC_ACQ_REL,
+                              __ATOMIC_ACQUIRE);
+  return expected;
+}
+inline uint64_t ld64(const void* p) { return __atomic_load_n(static_cast<const uint64_t*>(p), __ATOMIC_ACQUIRE); }
+inline void st64(void* p, uint64_t v) { __atomic_store_n(static_cast<uint64_t*>(p), v, __ATOMIC_RELEASE); }
+inline uint64_t add64(void* p, uint64_t v) { return __atomic_fetch_add(static_cast<uint64_t*>(p), v, __ATOMIC_ACQ_REL); }
+
+int itemsize(int dt) {
+  switch (dt) {
+    case VPE_F32: return 4;
+    case VPE_F16_RAW: return 2;
+    case VPE_U8: return 1;
+    case VPE_I32: return 4;
+    case VPE_I64: return 8;
+    case VPE_BF16: return 2;
+    default: return 0;
+  }
+}
+
+size_t align_up(size_t n, size_t a) { return (n + a - 1) / a * a; }
+
+}  // namespace
+
+struct vpe_ring {
+  int nspecs = 0, capacity = 0, mode = 0, device = 0;
+  vpe_tensor_spec* specs = nullptr;
+  size_t* nbytes = nullptr;   // per label
+  size_t* offsets = nullptr;  // [capacity * nspecs], data-area relative (ArenaLayout)
+  uint8_t* hdr = nullptr;
+  size_t hdr_bytes = 0;
+  uint8_t* data = nullptr;  // region base (64-byte PEAR1 header, then the data area)
+  size_t data_bytes = 0;
+  cudaEvent_t* ready = nullptr;       // [capacity]
+  cudaEvent_t* done = nullptr;        // [capacity * MAX_CONSUMERS]
+  uint8_t* done_valid = nullptr;      // [capacity * MAX_CONSUMERS]
+  int64_t* pending_evict = nullptr;   // [capacity], -1 none
+  uint64_t last_id = 0, last_ts = 0;
+  int cursor_slot[VPE_MAX_CONSUMERS];
+  uint32_t cursor_ids[VPE_MAX_CONSUMERS];
+  int ncursor_cache = 0;
+
+  uint8_t* state(int i) { return hdr + SLOT0 + i * SLOT_STRIDE; }
+  uint8_t* fid(int i) { return hdr + SLOT0 + i * SLOT_STRIDE + 8; }
+  uint8_t* ts(int i) { return hdr + SLOT0 + i * SLOT_STRIDE + 16; }
+  uint8_t* cursor(int idx) { return hdr + SLOT0 + capacity * SLOT_STRIDE + idx * CURSOR_STRIDE; }
+  uint8_t* drops() { return cursor(VPE_MAX_CONSUMERS); }
+  uint8_t* evictions() { return drops() + 8; }
+  uint8_t* pushed() { return drops() + 16; }
+  uint8_t* consumed() { return drops() + 24; }
+  uint8_t* slot_ptr(int slot, int label) { return data + ARENA_HDR + offsets[slot * nspecs + label]; }
+  int cursor_idx(uint32_t cid) const {
+    for (int i = 0; i < ncursor_cache; ++i)
+      if (cursor_ids[i] == cid) return cursor_slot[i];
+    return -1;
+  }
+};
+
+static size_t header_region_bytes(int capacity) {
+  const size_t need = SLOT0 + (size_t)capacity * SLOT_STRIDE + VPE_MAX_CONSUMERS * CURSOR_STRIDE + 32;
+  return std::max<size_t>(4096, align_up(need, 4096));
+}
+
+extern "C" {
+
+int64_t vpe_copy_counter(void) { return g_copies.load(); }
+
+int64_t vpe_now_ns(void) {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+void vpe_busy_spin_ns(int64_t ns) {
+  if (ns <= 0) return;
+  const int64_t end = vpe_now_ns() + ns;
+  while (vpe_now_ns() < end) {
+  }
+}
+
+// ---- AtomicBuffer replacement (_kernels.pyx:56-98): same offset checks, same orders ----
+int vpe_atomic_check_base(const void* base, size_t size) {
+  if (size > 0 && reinterpret_cast<uintptr_t>(base) % 8 != 0) return VPE_E_VALUE;
+  return VPE_OK;
+}
+static inline bool bad(size_t size, int64_t off, int w) { return off < 0 || off + w > (int64_t)size || off % w; }
+int vpe_u32_load(void* b, size_t size, int64_t off, uint32_t* out) {
+  if (bad(size, off, 4)) return VPE_E_VALUE;
+  *out = ld32(static_cast<uint8_t*>(b) + off);
+  return VPE_OK;
+}
+int vpe_u32_store(void* b, size_t size, int64_t off, uint32_t v) {
+  if (bad(size, off, 4)) return VPE_E_VALUE;
+  st32(static_cast<uint8_t*>(b) + off, v);
+  return VPE_OK;
+}
+int vpe_u32_cas(void* b, size_t size, int64_t off, uint32_t e, uint32_t d, uint32_t* prev) {
+  if (bad(size, off, 4)) return VPE_E_VALUE;
+  *prev = cas32(static_cast<uint8_t*>(b) + off, e, d);
+  return VPE_OK;
+}
+int vpe_u64_load(void* b, size_t size, int64_t off, uint64_t* out) {
+  if (bad(size, off, 8)) return VPE_E_VALUE;
+  *out = ld64(static_cast<uint8_t*>(b) + off);
+  return VPE_OK;
+}
+int vpe_u64_store(void* b, size_t size, int64_t off, uint64_t v) {
+  if (bad(size, off, 8)) return VPE_E_VALUE;
+  st64(static_cast<uint8_t*>(b) + off, v);
+  return VPE_OK;
+}
+int vpe_u64_add(void* b, size_t size, int64_t off, uint64_t d, uint64_t* prev) {
+  if (bad(size, off, 8)) return VPE_E_VALUE;
+  *prev = add64(static_cast<uint8_t*>(b) + off, d);
+  return VPE_OK;
+}
+
+// ---- ring ----
+int vpe_ring_destroy(vpe_ring* r) {
+  if (!r) return VPE_OK;
+  if (r->ready)
+    for (int i = 0; i < r->capacity; ++i)
+      if (r->ready[i]) cudaEventDestroy(r->ready[i]);
+  if (r->done)
+    for (int i = 0; i < r->capacity * VPE_MAX_CONSUMERS; ++i)
+      if (r->done[i]) cudaEventDestroy(r->done[i]);
+  if (r->data) {
+    if (r->device == VPE_HOST_PINNED)
+      cudaFreeHost(r->data);
+    else
+      cudaFree(r->data);
+  }
+  free(r->hdr);
+  delete[] r->specs;
+  delete[] r->nbytes;
+  delete[] r->offsets;
+  delete[] r->ready;
+  delete[] r->done;
+  delete[] r->done_valid;
+  delete[] r->pending_evict;
+  delete r;
+  return VPE_OK;
+}
+
+int vpe_ring_create(const vpe_tensor_spec* specs, int32_t nspecs, int32_t capacity, int32_t mode, int32_t device,
+                    vpe_ring** out) {
+  if (!out) return VPE_E_VALUE;
+  if (capacity < 2) return VPE_E_CONFIG;  // channels.py:547-548
+  if (nspecs < 1 || !specs) return VPE_E_CONFIG;
+  if (mode != VPE_FIFO && mode != VPE_LATEST) return VPE_E_CONFIG;
+  for (int i = 0; i < nspecs; ++i) {
+    if (itemsize(specs[i].dtype) == 0 || specs[i].rank < 1 || specs[i].rank > 4) return VPE_E_SHAPE;
+    for (int d = 0; d < specs[i].rank; ++d)
+      if (specs[i].dims[d] <= 0) return VPE_E_SHAPE;
+    for (int j = 0; j < i; ++j)
+      if (strncmp(specs[i].label, specs[j].label, 64) == 0) return VPE_E_CONFIG;
+  }
+  vpe_ring* r = new (std::nothrow) vpe_ring();
+  if (!r) return VPE_E_RESOURCE;
+  r->nspecs = nspecs;
+  r->capacity = capacity;
+  r->mode = mode;
+  r->device = device;
+  r->specs = new vpe_tensor_spec[nspecs];
+  memcpy(r->specs, specs, sizeof(vpe_tensor_spec) * nspecs);
+  r->nbytes = new size_t[nspecs];
+  for (int i = 0; i < nspecs; ++i) {
+    size_t n = itemsize(specs[i].dtype);
+    for (int d = 0; d < specs[i].rank; ++d) n *= (size_t)specs[i].dims[d];
+    r->nbytes[i] = n;
+  }
+  // ArenaLayout.from_specs(specs * capacity): 64-byte aligned, in order (arena.py:114-126)
+  r->offsets = new size_t[(size_t)nspecs * capacity];
+  size_t cur = 0;
+  for (int s = 0; s < capacity; ++s)
+    for (int l = 0; l < nspecs; ++l) {
+      const size_t off = align_up(cur, ALIGN);
+      r->offsets[s * nspecs + l] = off;
+      cur = off + r->nbytes[l];
+    }
+  r->data_bytes = align_up(ARENA_HDR + cur, 4096);
+  r->hdr_bytes = header_region_bytes(capacity);
+  r->hdr = static_cast<uint8_t*>(aligned_alloc(4096, r->hdr_bytes));
+  r->ready = new cudaEvent_t[capacity]();
+  r->done = new cudaEvent_t[(size_t)capacity * VPE_MAX_CONSUMERS]();
+  r->done_valid = new uint8_t[(size_t)capacity * VPE_MAX_CONSUMERS]();
+  r->pending_evict = new int64_t[capacity];
+  if (!r->hdr) {
+    vpe_ring_destroy(r);
+    return VPE_E_RESOURCE;
+  }
+  memset(r->hdr, 0, r->hdr_bytes);
+  memcpy(r->hdr, "PECH1\0", 6);
+  r->hdr[6] = (uint8_t)mode;
+  uint32_t cap = capacity;
+  memcpy(r->hdr + 8, &cap, 4);
+  for (int i = 0; i < capacity; ++i) r->pending_evict[i] = -1;
+  cudaError_t e;
+  if (device == VPE_HOST_PINNED) {
+    e = cudaHostAlloc(reinterpret_cast<void**>(&r->data), r->data_bytes, cudaHostAllocPortable);
+    if (e == cudaSuccess) memset(r->data, 0, r->data_bytes);
+  } else {
+    e = cudaMalloc(reinterpret_cast<void**>(&r->data), r->data_bytes);
+    if (e == cudaSuccess) e = cudaMemset(r->data, 0, r->data_bytes);
+  }
+  if (e != cudaSuccess) {
+    r->data = nullptr;
+    vpe_ring_destroy(r);
+    return VPE_E_RESOURCE;
+  }
+  // PEAR1 region header (arena.py:322-324)
+  uint8_t h[ARENA_HDR] = {0};
+  memcpy(h, "PEAR1\0", 6);
+  uint64_t tb = r->data_bytes;
+  memcpy(h + 8, &tb, 8);
+  uint32_t nslots = (uint32_t)(nspecs * capacity);
+  memcpy(h + 16, &nslots, 4);
+  if (cudaMemcpy(r->data, h, ARENA_HDR, cudaMemcpyDefault) != cudaSuccess) {
+    vpe_ring_destroy(r);
+    return VPE_E_CUDA;
+  }
+  for (int i = 0; i < capacity; ++i)
+    if (cudaEventCreateWithFlags(&r->ready[i], cudaEventDisableTiming) != cudaSuccess) {
+      vpe_ring_destroy(r);
+      return VPE_E_CUDA;
+    }
+  for (int i = 0; i < capacity * VPE_MAX_CONSUMERS; ++i)
+    if (cudaEventCreateWithFlags(&r->done[i], cudaEventDisableTiming) != cudaSuccess) {
+      vpe_ring_destroy(r);
+      return VPE_E_CUDA;
+    }
+  *out = r;
+  return VPE_OK;
+}
+
+int vpe_ring_header(vpe_ring* r, void** base, size_t* size) {
+  if (!r) return VPE_E_VALUE;
+  *base = r->hdr;
+  *size = r->hdr_bytes;
+  return VPE_OK;
+}
+int vpe_ring_data(vpe_ring* r, void** base, size_t* size) {
+  if (!r) return VPE_E_VALUE;
+  *base = r->data;
+  *size = r->data_bytes;
+  return VPE_OK;
+}
+int vpe_ring_slot_ptr(vpe_ring* r, int32_t slot, int32_t label, void** ptr) {
+  if (!r || slot < 0 || slot >= r->capacity) return VPE_E_NOT_FOUND;
+  if (label < 0 || label >= r->nspecs) return VPE_E_LABEL;
+  *ptr = r->slot_ptr(slot, label);
+  return VPE_OK;
+}
+int vpe_ring_label_offset(vpe_ring* r, int32_t slot, int32_t label, int64_t* off) {
+  if (!r || slot < 0 || slot >= r->capacity) return VPE_E_NOT_FOUND;
+  if (label < 0 || label >= r->nspecs) return VPE_E_LABEL;
+  *off = (int64_t)r->offsets[slot * r->nspecs + label];
+  return VPE_OK;
+}
+
+// channels.py:311-331 _claim_slot
+static int claim_slot(vpe_ring* r, int* slot, int64_t* evicted) {
+  for (;;) {
+    for (int i = 0; i < r->capacity; ++i)
+      if (ld32(r->state(i)) == STATE_FREE && cas32(r->state(i), STATE_FREE, STATE_WRITING) == STATE_FREE) {
+        *slot = i;
+        *evicted = -1;
+        return VPE_OK;
+      }
+    if (r->mode == VPE_FIFO) return VPE_OVERFLOW_REJECTED;
+    int oldest = -1;
+    uint64_t oldest_fid = 0;
+    for (int i = 0; i < r->capacity; ++i)
+      if (ld32(r->state(i)) == STATE_READY) {
+        const uint64_t f = ld64(r->fid(i));
+        if (oldest < 0 || f < oldest_fid) {
+          oldest = i;
+          oldest_fid = f;
+        }
+      }
+    if (oldest < 0) return VPE_OVERFLOW_REJECTED;
+    if (cas32(r->state(oldest), STATE_READY, STATE_WRITING) == STATE_READY) {
+      *slot = oldest;
+      *evicted = (int64_t)oldest_fid;
+      return VPE_OK;
+    }
+  }
+}
+
+int vpe_ring_claim(vpe_ring* r, uint64_t frame_id, uint64_t capture_ts, void* stream, int32_t* slot,
+                   uint64_t* evicted_fid, int32_t* evicted) {
+  if (!r || !slot) return VPE_E_VALUE;
+  if (frame_id <= r->last_id) return VPE_E_VALUE;  // channels.py:284-285
+  if (capture_ts < r->last_ts) return VPE_E_VALUE; // channels.py:286-287
+  int s;
+  int64_t ev;
+  const int rc = claim_slot(r, &s, &ev);
+  if (rc == VPE_OVERFLOW_REJECTED) {
+    add64(r->drops(), 1);
+    add64(r->pushed(), 1);
+    return rc;
+  }
+  st64(r->fid(s), frame_id);
+  st64(r->ts(s), capture_ts);
+  r->pending_evict[s] = ev;
+  if (evicted) *evicted = ev >= 0;
+  if (evicted_fid) *evicted_fid = ev >= 0 ? (uint64_t)ev : 0;
+  *slot = s;
+  // WAR: the new writes must not start before every earlier reader of this slot finished
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int c = 0; c < VPE_MAX_CONSUMERS; ++c) {
+    const int k = s * VPE_MAX_CONSUMERS + c;
+    if (r->done_valid[k]) VPE_CUDA_TRY(cudaStreamWaitEvent(st, r->done[k], 0));
+  }
+  return VPE_OK;
+}
+
+int vpe_ring_publish(vpe_ring* r, int32_t slot, void* stream) {
+  if (!r || slot < 0 || slot >= r->capacity) return VPE_E_NOT_FOUND;
+  if (ld32(r->state(slot)) != STATE_WRITING) return VPE_E_RUNTIME;
+  VPE_CUDA_TRY(cudaEventRecord(r->ready[slot], static_cast<cudaStream_t>(stream)));
+  r->last_id = ld64(r->fid(slot));
+  r->last_ts = ld64(r->ts(slot));
+  st32(r->state(slot), STATE_READY);
+  add64(r->pushed(), 1);
+  if (r->pending_evict[slot] >= 0) add64(r->evictions(), 1);
+  r->pending_evict[slot] = -1;
+  return VPE_OK;
+}
+
+int vpe_ring_abort(vpe_ring* r, int32_t slot) {
+  if (!r || slot < 0 || slot >= r->capacity) return VPE_E_NOT_FOUND;
+  r->pending_evict[slot] = -1;
+  st32(r->state(slot), STATE_FREE);  // channels.py:299-301
+  return VPE_OK;
+}
+
+// channels.py:335-358
+int vpe_ring_register_consumer(vpe_ring* r, uint32_t cid, int32_t* warn) {
+  if (!r) return VPE_E_VALUE;
+  if (warn) *warn = 0;
+  if (cid < 1 || cid > 0xFFFFFFFEu) return VPE_E_CONFIG;
+  int registered = 0;
+  for (int idx = 0; idx < VPE_MAX_CONSUMERS; ++idx) {
+    const uint32_t cur = ld32(r->cursor(idx));
+    if (cur == cid) {
+      if (r->cursor_idx(cid) < 0) {
+        r->cursor_ids[r->ncursor_cache] = cid;
+        r->cursor_slot[r->ncursor_cache++] = idx;
+      }
+      return VPE_OK;
+    }
+    if (cur != 0) ++registered;
+  }
+  for (int idx = 0; idx < VPE_MAX_CONSUMERS; ++idx)
+    if (ld32(r->cursor(idx)) == 0 && cas32(r->cursor(idx), 0, cid) == 0) {
+      r->cursor_ids[r->ncursor_cache] = cid;
+      r->cursor_slot[r->ncursor_cache++] = idx;
+      if (warn && r->mode == VPE_LATEST && registered + 2 > r->capacity) *warn = 1;
+      return VPE_OK;
+    }
+  return VPE_E_RESOURCE;
+}
+
+int vpe_ring_last_consumed(vpe_ring* r, uint32_t cid, uint64_t* fid) {
+  if (!r) return VPE_E_VALUE;
+  const int idx = r->cursor_idx(cid);
+  if (idx < 0) return VPE_E_NOT_FOUND;
+  *fid = ld64(r->cursor(idx) + 8);
+  return VPE_OK;
+}
+
+// channels.py:423-452
+int vpe_ring_acquire_latest(vpe_ring* r, uint32_t cid, void* stream, vpe_lease* lease) {
+  if (!r || !lease) return VPE_E_VALUE;
+  const int cidx = r->cursor_idx(cid);
+  if (cidx < 0) return VPE_E_NOT_FOUND;
+  const uint64_t cursor = ld64(r->cursor(cidx) + 8);
+  for (;;) {
+    int best = -1;
+    uint64_t best_fid = cursor;
+    uint32_t best_state = 0;
+    for (int i = 0; i < r->capacity; ++i) {
+      const uint32_t st = ld32(r->state(i));
+      if (st >= STATE_READY) {
+        const uint64_t f = ld64(r->fid(i));
+        if (f > best_fid) {
+          best = i;
+          best_fid = f;
+          best_state = st;
+        }
+      }
+    }
+    if (best < 0) return VPE_NO_NEW_DATA;
+    uint32_t st = best_state;
+    while (st >= STATE_READY) {
+      const uint32_t prev = cas32(r->state(best), st, st + 1);
+      if (prev == st) {
+        lease->slot = best;
+        lease->consumer_id = cid;
+        lease->frame_id = ld64(r->fid(best));
+        lease->capture_ts = ld64(r->ts(best));
+        lease->consumed = 0;
+        if (stream) VPE_CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), r->ready[best], 0));
+        return VPE_OK;
+      }
+      st = prev;
+    }
+  }
+}
+
+// channels.py:483-489
+static int release_slot(vpe_ring* r, int slot) {
+  for (;;) {
+    const uint32_t st = ld32(r->state(slot));
+    if (st <= STATE_READY) return VPE_E_RUNTIME;
+    if (cas32(r->state(slot), st, st - 1) == st) return VPE_OK;
+  }
+}
+
+static int finish(vpe_ring* r, vpe_lease* lease, void* stream) {
+  const int cidx = r->cursor_idx(lease->consumer_id);
+  if (cidx < 0) return VPE_E_NOT_FOUND;
+  const int k = lease->slot * VPE_MAX_CONSUMERS + cidx;
+  if (stream) {
+    VPE_CUDA_TRY(cudaEventRecord(r->done[k], static_cast<cudaStream_t>(stream)));
+    r->done_valid[k] = 1;
+  }
+  st64(r->cursor(cidx) + 8, lease->frame_id);  // channels.py:470
+  add64(r->consumed(), 1);
+  VPE_TRY(release_slot(r, lease->slot));
+  lease->consumed = 1;
+  return VPE_OK;
+}
+
+int vpe_ring_commit(vpe_ring* r, vpe_lease* lease, void* stream) {
+  if (!r || !lease) return VPE_E_VALUE;
+  if (lease->consumed) return VPE_E_USE_AFTER_CONSUME;
+  return finish(r, lease, stream);
+}
+
+int vpe_ring_consume(vpe_ring* r, vpe_lease* lease, const int32_t* labels, int32_t nlabels, void* const* dst,
+                     void* stream) {
+  if (!r || !lease) return VPE_E_VALUE;
+  if (lease->consumed) return VPE_E_USE_AFTER_CONSUME;  // channels.py:459-460
+  for (int i = 0; i < nlabels; ++i)
+    if (labels[i] < 0 || labels[i] >= r->nspecs) return VPE_E_LABEL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < nlabels; ++i) {
+    VPE_CUDA_TRY(cudaMemcpyAsync(dst[i], r->slot_ptr(lease->slot, labels[i]), r->nbytes[labels[i]], cudaMemcpyDefault,
+                                 st));
+    g_copies.fetch_add(1);
+  }
+  return finish(r, lease, stream);
+}
+
+int vpe_ring_release(vpe_ring* r, vpe_lease* lease, void* stream) {
+  if (!r || !lease) return VPE_E_VALUE;
+  if (lease->consumed) return VPE_OK;  // channels.py:478-479
+  if (stream) {
+    const int cidx = r->cursor_idx(lease->consumer_id);
+    if (cidx >= 0) {
+      const int k = lease->slot * VPE_MAX_CONSUMERS + cidx;
+      VPE_CUDA_TRY(cudaEventRecord(r->done[k], static_cast<cudaStream_t>(stream)));
+      r->done_valid[k] = 1;
+    }
+  }
+  VPE_TRY(release_slot(r, lease->slot));
+  lease->consumed = 1;
+  return VPE_OK;
+}
+
+// channels.py:377-421
+int vpe_ring_pop(vpe_ring* r, uint32_t cid, void* const* dst, void* stream, vpe_lease* env) {
+  if (!r) return VPE_E_VALUE;
+  if (r->mode != VPE_FIFO) return VPE_E_CONFIG;
+  const int cidx = r->cursor_idx(cid);
+  if (cidx < 0) return VPE_E_NOT_FOUND;
+  for (;;) {
+    int best = -1;
+    uint64_t best_fid = 0;
+    for (int i = 0; i < r->capacity; ++i)
+      if (ld32(r->state(i)) == STATE_READY) {
+        const uint64_t f = ld64(r->fid(i));
+        if (best < 0 || f < best_fid) {
+          best = i;
+          best_fid = f;
+        }
+      }
+    if (best < 0) return VPE_NO_NEW_DATA;
+    if (cas32(r->state(best), STATE_READY, STATE_READY + 1) != STATE_READY) continue;
+    const uint64_t fid = ld64(r->fid(best));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (st) {
+      VPE_CUDA_TRY(cudaStreamWaitEvent(st, r->ready[best], 0));
+      for (int l = 0; l < r->nspecs; ++l) {
+        VPE_CUDA_TRY(cudaMemcpyAsync(dst[l], r->slot_ptr(best, l), r->nbytes[l], cudaMemcpyDefault, st));
+        g_copies.fetch_add(1);
+      }
+      const int k = best * VPE_MAX_CONSUMERS + cidx;
+      VPE_CUDA_TRY(cudaEventRecord(r->done[k], st));
+      r->done_valid[k] = 1;
+    } else {
+      // host consumer: wait for the producer's writes, then copy on the host
+      VPE_CUDA_TRY(cudaEventSynchronize(r->ready[best]));
+      for (int l = 0; l < r->nspecs; ++l) {
+        if (r->device == VPE_HOST_PINNED)
+          memcpy(dst[l], r->slot_ptr(best, l), r->nbytes[l]);
+        else
+          VPE_CUDA_TRY(cudaMemcpy(dst[l], r->slot_ptr(best, l), r->nbytes[l], cudaMemcpyDefault));
+        g_copies.fetch_add(1);
+      }
+    }
+    if (env) {
+      env->slot = best;
+      env->consumer_id = cid;
+      env->frame_id = fid;
+      env->capture_ts = ld64(r->ts(best));
+      env->consumed = 1;
+    }
+    st64(r->cursor(cidx) + 8, fid);
+    add64(r->consumed(), 1);
+    st32(r->state(best), STATE_FREE);
+    return VPE_OK;
+  }
+}
+
+int vpe_ring_counters(vpe_ring* r, vpe_counters* c) {
+  if (!r || !c) return VPE_E_VALUE;
+  uint64_t resident = 0;
+  for (int i = 0; i < r->capacity; ++i)
+    if (ld32(r->state(i)) >= STATE_READY) ++resident;
+  c->pushed = ld64(r->pushed());
+  c->producer_drops = ld64(r->drops());
+  c->evictions = ld64(r->evictions());
+  c->consumed = ld64(r->consumed());
+  c->resident = resident;
+  return VPE_OK;
+}
+
+int vpe_ring_slot_state(vpe_ring* r, int32_t slot, uint32_t* state, uint64_t* fid) {
+  if (!r || slot < 0 || slot >= r->capacity) return VPE_E_NOT_FOUND;
+  *state = ld32(r->state(slot));
+  *fid = ld64(r->fid(slot));
+  return VPE_OK;
+}
+
+}  // extern "C"

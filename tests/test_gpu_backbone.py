@@ -1,0 +1,36 @@
+"""Backbone parity on the B200 vs the fp32 CPU oracle (north-star tolerance: rel-L2 <= 1e-2,
+cosine >= 0.999 per tap)."""
+
+import pytest
+import torch
+
+from oracle import vit as ovit
+from paper_2508_11584_b200.config import model_config, tokens
+from paper_2508_11584_b200.weights import make_frames, make_weights
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm()).item()
+
+
+def cosine(a, b):
+    return torch.nn.functional.cosine_similarity(a.float().flatten(), b.float().flatten(), dim=0).item()
+
+
+@pytest.mark.parametrize("R,B", [(224, 1), (448, 1), (224, 3)])
+def test_backbone_taps_vs_oracle(device, R, B):
+    from paper_2508_11584_b200.backbone import Backbone
+    cfg = model_config("vits14")
+    W = make_weights("vits14", heads=())
+    frames = make_frames(B, R, 0)
+    bb = Backbone(W, cfg.backbone, R, B, device)
+    T = tokens(R)
+    taps = [torch.empty(B, T, cfg.backbone.dim, device=device, dtype=torch.bfloat16) for _ in range(4)]
+    bb.forward(frames.to(device), taps)
+    torch.cuda.synchronize()
+    ref = ovit.backbone_forward(frames, W, cfg.backbone.depth, cfg.backbone.heads, cfg.backbone.taps)
+    for k, (g, r) in enumerate(zip(taps, ref)):
+        e, c = rel_l2(g.cpu(), r), cosine(g.cpu(), r)
+        assert e <= 1e-2 and c >= 0.999, f"tap {k}: rel-L2 {e:.3e} cos {c:.6f}"

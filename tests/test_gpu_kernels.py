@@ -1,0 +1,115 @@
+"""Kernel-level parity on the B200: each sm_100a kernel vs a plain torch fp32 reference of the
+same op on the same bf16-rounded inputs. Tolerances are stated per test."""
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    a, b = a.float(), b.float()
+    return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    from paper_2508_11584_b200 import _ops
+    return _ops
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 64, 64, 64), (1025, 1152, 384, 128), (1025, 384, 1536, 64),
+                                      (300, 200, 128, 32), (4100, 1536, 384, 256), (257, 96, 192, 64)])
+def test_linear_bf16(ops, device, M, N, K, bn):
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    a = torch.randn(M, K, generator=g).to(device, torch.bfloat16)
+    w = (torch.randn(N, K, generator=g) * 0.05).to(device, torch.bfloat16)
+    bias = torch.randn(N, generator=g).to(device)
+    out = ops.linear(a, w, bias=bias, bn=bn)
+    torch.cuda.synchronize()
+    ref = a.float() @ w.float().t() + bias
+    assert rel_l2(out, ref) < 8e-3  # bf16 output rounding
+
+
+def test_linear_gelu_and_resid(ops, device):
+    g = torch.Generator().manual_seed(1)
+    M, N, K = 1025, 1536, 384
+    a = torch.randn(M, K, generator=g).to(device, torch.bfloat16)
+    w = (torch.randn(N, K, generator=g) * 0.05).to(device, torch.bfloat16)
+    bias = torch.randn(N, generator=g).to(device)
+    out = ops.linear(a, w, bias=bias, act=ops.ACT_GELU, bn=128)
+    ref = F.gelu(a.float() @ w.float().t() + bias)
+    assert rel_l2(out, ref) < 8e-3
+    # residual + layerscale into fp32 stream
+    w2 = (torch.randn(384, N, generator=g) * 0.02).to(device, torch.bfloat16)
+    b2 = torch.randn(384, generator=g).to(device)
+    ls = torch.rand(384, generator=g).to(device) + 0.5
+    h = torch.randn(M, 384, generator=g).to(device)
+    h0 = h.clone()
+    ops.linear(out, w2, bias=b2, scale=ls, out=h, kind=ops.EPI_RESID, bn=64)
+    ref2 = h0 + ls * (out.float() @ w2.float().t() + b2)
+    torch.cuda.synchronize()
+    assert rel_l2(h, ref2) < 1e-5
+
+
+def test_linear_split_precision(ops, device):
+    """A (exact bf16) x (W_hi + W_lo) ~ fp32-accurate weights (seg/det heads)."""
+    g = torch.Generator().manual_seed(2)
+    M, N, K = 1024, 160, 384
+    a = torch.randn(M, K, generator=g).to(torch.bfloat16)
+    w = torch.randn(N, K, generator=g) * 0.05
+    hi = w.to(torch.bfloat16)
+    lo = (w - hi.float()).to(torch.bfloat16)
+    ws = torch.cat([hi, lo], 1).to(device)
+    out = ops.linear(a.to(device), ws, kind=ops.EPI_F32, bn=32)
+    ref = a.double() @ w.double().t()
+    assert rel_l2(out.cpu().double(), ref) < 1e-5
+
+
+@pytest.mark.parametrize("B,T,heads", [(1, 257, 6), (1, 1025, 6), (2, 1370, 12), (1, 128, 2), (3, 200, 4)])
+def test_attention(ops, device, B, T, heads):
+    D = heads * 64
+    g = torch.Generator().manual_seed(T)
+    qkv = torch.randn(B * T, 3 * D, generator=g).to(device, torch.bfloat16)
+    out = ops.attention(qkv, B, T, D, heads)
+    q, k, v = qkv.float().view(B, T, 3, heads, 64).permute(2, 0, 3, 1, 4)
+    ref = torch.softmax(q @ k.transpose(-1, -2) / 8.0, -1) @ v
+    ref = ref.transpose(1, 2).reshape(B * T, D)
+    torch.cuda.synchronize()
+    assert rel_l2(out, ref) < 1.5e-2
+
+
+def test_layernorm(ops, device):
+    g = torch.Generator().manual_seed(3)
+    x = (torch.randn(1025, 384, generator=g) * 3 + 1).to(device)
+    w, b = torch.randn(384, generator=g).to(device), torch.randn(384, generator=g).to(device)
+    w2, b2 = torch.randn(384, generator=g).to(device), torch.randn(384, generator=g).to(device)
+    o1, o2 = ops.layernorm(x, w, b, 1e-6, w2, b2)
+    torch.cuda.synchronize()
+    assert rel_l2(o1, F.layer_norm(x, (384,), w, b, 1e-6)) < 5e-3
+    assert rel_l2(o2, F.layer_norm(x, (384,), w2, b2, 1e-6)) < 5e-3
+
+
+@pytest.mark.parametrize("H,W,C,Cp,N,ks", [(16, 16, 64, 64, 64, 3), (32, 32, 48, 64, 64, 3), (64, 64, 96, 128, 64, 3),
+                                           (448, 448, 32, 32, 32, 3), (37, 37, 64, 64, 64, 3), (32, 32, 384, 384, 192, 1)])
+def test_conv_nhwc(ops, device, H, W, C, Cp, N, ks):
+    g = torch.Generator().manual_seed(H + C)
+    B = 2 if H < 100 else 1
+    x = torch.zeros(B, H, W, Cp)
+    x[..., :C] = torch.randn(B, H, W, C, generator=g)
+    w = torch.randn(N, C, ks, ks, generator=g) * 0.05
+    bias = torch.randn(N, generator=g)
+    add1 = torch.randn(B, H, W, N, generator=g)
+    wk = torch.zeros(N, ks, ks, Cp)
+    wk[..., :C] = w.permute(0, 2, 3, 1)
+    xd = x.to(device, torch.bfloat16)
+    out = ops.conv(xd, wk.reshape(N, -1).to(device, torch.bfloat16), C, ks, bias=bias.to(device),
+                   add1=add1.to(device, torch.bfloat16), act=ops.ACT_RELU)
+    ref = F.conv2d(xd.float()[..., :C].permute(0, 3, 1, 2), w.to(torch.bfloat16).float().to(device),
+                   bias.to(device), padding=ks // 2).permute(0, 2, 3, 1)
+    ref = F.relu(ref + add1.to(device, torch.bfloat16).float())
+    torch.cuda.synchronize()
+    assert rel_l2(out, ref) < 8e-3
