@@ -62,6 +62,7 @@ enum { VPE_F32 = 0, VPE_F16_RAW = 1, VPE_U8 = 2, VPE_I32 = 3, VPE_I64 = 4, VPE_B
 enum { VPE_FIFO = 0, VPE_LATEST = 1 };               /* ChannelMode, channels.py:68-70 */
 #define VPE_MAX_CONSUMERS 16                         /* channels.py:58 */
 #define VPE_HOST_PINNED (-1)                         /* ring data in pinned host memory */
+#define VPE_HOST_PLAIN (-2)                          /* ring data in pageable host memory, no CUDA (tests) */
 
 /* ---- atomics over a caller-owned buffer (replaces fanpipe._kernels.AtomicBuffer) ---- */
 int vpe_atomic_check_base(const void* base, size_t size);

@@ -160,7 +160,9 @@ int vpe_ring_destroy(vpe_ring* r) {
     for (int i = 0; i < r->capacity * VPE_MAX_CONSUMERS; ++i)
       if (r->done[i]) cudaEventDestroy(r->done[i]);
   if (r->data) {
-    if (r->device == VPE_HOST_PINNED)
+    if (r->device == VPE_HOST_PLAIN)
+      free(r->data);
+    else if (r->device == VPE_HOST_PINNED)
       cudaFreeHost(r->data);
     else
       cudaFree(r->data);
@@ -230,8 +232,13 @@ int vpe_ring_create(const vpe_tensor_spec* specs, int32_t nspecs, int32_t capaci
   uint32_t cap = capacity;
   memcpy(r->hdr + 8, &cap, 4);
   for (int i = 0; i < capacity; ++i) r->pending_evict[i] = -1;
-  cudaError_t e;
-  if (device == VPE_HOST_PINNED) {
+  cudaError_t e = cudaSuccess;
+  const bool plain = device == VPE_HOST_PLAIN;
+  if (plain) {
+    r->data = static_cast<uint8_t*>(aligned_alloc(4096, r->data_bytes));
+    if (r->data) memset(r->data, 0, r->data_bytes);
+    else e = cudaErrorMemoryAllocation;
+  } else if (device == VPE_HOST_PINNED) {
     e = cudaHostAlloc(reinterpret_cast<void**>(&r->data), r->data_bytes, cudaHostAllocPortable);
     if (e == cudaSuccess) memset(r->data, 0, r->data_bytes);
   } else {
@@ -250,6 +257,11 @@ int vpe_ring_create(const vpe_tensor_spec* specs, int32_t nspecs, int32_t capaci
   memcpy(h + 8, &tb, 8);
   uint32_t nslots = (uint32_t)(nspecs * capacity);
   memcpy(h + 16, &nslots, 4);
+  if (plain) {
+    memcpy(r->data, h, ARENA_HDR);
+    *out = r;
+    return VPE_OK;  // host-only ring: no CUDA events, streams must be NULL
+  }
   if (cudaMemcpy(r->data, h, ARENA_HDR, cudaMemcpyDefault) != cudaSuccess) {
     vpe_ring_destroy(r);
     return VPE_E_CUDA;
@@ -343,17 +355,19 @@ int vpe_ring_claim(vpe_ring* r, uint64_t frame_id, uint64_t capture_ts, void* st
   *slot = s;
   // WAR: the new writes must not start before every earlier reader of this slot finished
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  for (int c = 0; c < VPE_MAX_CONSUMERS; ++c) {
-    const int k = s * VPE_MAX_CONSUMERS + c;
-    if (r->done_valid[k]) VPE_CUDA_TRY(cudaStreamWaitEvent(st, r->done[k], 0));
-  }
+  if (r->device != VPE_HOST_PLAIN)
+    for (int c = 0; c < VPE_MAX_CONSUMERS; ++c) {
+      const int k = s * VPE_MAX_CONSUMERS + c;
+      if (r->done_valid[k]) VPE_CUDA_TRY(cudaStreamWaitEvent(st, r->done[k], 0));
+    }
   return VPE_OK;
 }
 
 int vpe_ring_publish(vpe_ring* r, int32_t slot, void* stream) {
   if (!r || slot < 0 || slot >= r->capacity) return VPE_E_NOT_FOUND;
   if (ld32(r->state(slot)) != STATE_WRITING) return VPE_E_RUNTIME;
-  VPE_CUDA_TRY(cudaEventRecord(r->ready[slot], static_cast<cudaStream_t>(stream)));
+  if (r->device != VPE_HOST_PLAIN)
+    VPE_CUDA_TRY(cudaEventRecord(r->ready[slot], static_cast<cudaStream_t>(stream)));
   r->last_id = ld64(r->fid(slot));
   r->last_ts = ld64(r->ts(slot));
   st32(r->state(slot), STATE_READY);
@@ -436,7 +450,8 @@ int vpe_ring_acquire_latest(vpe_ring* r, uint32_t cid, void* stream, vpe_lease* 
         lease->frame_id = ld64(r->fid(best));
         lease->capture_ts = ld64(r->ts(best));
         lease->consumed = 0;
-        if (stream) VPE_CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), r->ready[best], 0));
+        if (stream && r->device != VPE_HOST_PLAIN)
+          VPE_CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), r->ready[best], 0));
         return VPE_OK;
       }
       st = prev;
@@ -457,7 +472,7 @@ static int finish(vpe_ring* r, vpe_lease* lease, void* stream) {
   const int cidx = r->cursor_idx(lease->consumer_id);
   if (cidx < 0) return VPE_E_NOT_FOUND;
   const int k = lease->slot * VPE_MAX_CONSUMERS + cidx;
-  if (stream) {
+  if (stream && r->device != VPE_HOST_PLAIN) {
     VPE_CUDA_TRY(cudaEventRecord(r->done[k], static_cast<cudaStream_t>(stream)));
     r->done_valid[k] = 1;
   }
@@ -482,8 +497,11 @@ int vpe_ring_consume(vpe_ring* r, vpe_lease* lease, const int32_t* labels, int32
     if (labels[i] < 0 || labels[i] >= r->nspecs) return VPE_E_LABEL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   for (int i = 0; i < nlabels; ++i) {
-    VPE_CUDA_TRY(cudaMemcpyAsync(dst[i], r->slot_ptr(lease->slot, labels[i]), r->nbytes[labels[i]], cudaMemcpyDefault,
-                                 st));
+    if (r->device == VPE_HOST_PLAIN)
+      memcpy(dst[i], r->slot_ptr(lease->slot, labels[i]), r->nbytes[labels[i]]);
+    else
+      VPE_CUDA_TRY(cudaMemcpyAsync(dst[i], r->slot_ptr(lease->slot, labels[i]), r->nbytes[labels[i]],
+                                   cudaMemcpyDefault, st));
     g_copies.fetch_add(1);
   }
   return finish(r, lease, stream);
@@ -492,7 +510,7 @@ int vpe_ring_consume(vpe_ring* r, vpe_lease* lease, const int32_t* labels, int32
 int vpe_ring_release(vpe_ring* r, vpe_lease* lease, void* stream) {
   if (!r || !lease) return VPE_E_VALUE;
   if (lease->consumed) return VPE_OK;  // channels.py:478-479
-  if (stream) {
+  if (stream && r->device != VPE_HOST_PLAIN) {
     const int cidx = r->cursor_idx(lease->consumer_id);
     if (cidx >= 0) {
       const int k = lease->slot * VPE_MAX_CONSUMERS + cidx;
@@ -526,7 +544,7 @@ int vpe_ring_pop(vpe_ring* r, uint32_t cid, void* const* dst, void* stream, vpe_
     if (cas32(r->state(best), STATE_READY, STATE_READY + 1) != STATE_READY) continue;
     const uint64_t fid = ld64(r->fid(best));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (st) {
+    if (st && r->device != VPE_HOST_PLAIN) {
       VPE_CUDA_TRY(cudaStreamWaitEvent(st, r->ready[best], 0));
       for (int l = 0; l < r->nspecs; ++l) {
         VPE_CUDA_TRY(cudaMemcpyAsync(dst[l], r->slot_ptr(best, l), r->nbytes[l], cudaMemcpyDefault, st));
@@ -537,9 +555,9 @@ int vpe_ring_pop(vpe_ring* r, uint32_t cid, void* const* dst, void* stream, vpe_
       r->done_valid[k] = 1;
     } else {
       // host consumer: wait for the producer's writes, then copy on the host
-      VPE_CUDA_TRY(cudaEventSynchronize(r->ready[best]));
+      if (r->device != VPE_HOST_PLAIN) VPE_CUDA_TRY(cudaEventSynchronize(r->ready[best]));
       for (int l = 0; l < r->nspecs; ++l) {
-        if (r->device == VPE_HOST_PINNED)
+        if (r->device == VPE_HOST_PINNED || r->device == VPE_HOST_PLAIN)
           memcpy(dst[l], r->slot_ptr(best, l), r->nbytes[l]);
         else
           VPE_CUDA_TRY(cudaMemcpy(dst[l], r->slot_ptr(best, l), r->nbytes[l], cudaMemcpyDefault));
