@@ -19,7 +19,7 @@ constexpr int SMEM_ATT = 1024 + TILE /*Q*/ + 2 * TILE /*K*/ + 2 * TILE /*V*/ + 2
 constexpr int S_COL = 0, O_COL = 128, TMEM_COLS = 256;
 }  // namespace
 
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, 2)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tqkv, __nv_bfloat16* __restrict__ out, int T, int D,
                         float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
@@ -135,27 +135,18 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(s_full, j & 1);
       tc_fence_after();
       const int kvalid = T - j * 128;  // keys >= kvalid are padding
-      float sv[128];
+      // pass 1: row max over the 128 scores (read from TMEM in 32-column chunks)
+      float mx = m_prev;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float t[32];
         tmem_ld32(lane_addr + S_COL + c * 32, t);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = (c * 32 + i < kvalid) ? t[i] * scale_log2 : -INFINITY;
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i < kvalid) mx = fmaxf(mx, t[i] * scale_log2);
       }
-      float mx = m_prev;
-#pragma unroll
-      for (int i = 0; i < 128; ++i) mx = fmaxf(mx, sv[i]);
-      const float alpha = exp2f(m_prev - mx);  // m_prev=-inf on first block -> 0
-      float rs = 0.f;
-#pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        sv[i] = exp2f(sv[i] - mx);
-        rs += sv[i];
-      }
-      l = l * alpha + rs;
-      m_prev = mx;
+      const float alpha = fast_exp2(m_prev - mx);  // m_prev=-inf on the first block -> 0
       // O_{j-1} must be consumed (and PV_{j-1} finished reading P) before P_j is written
       if (j > 0) {
         mbar_wait(o_full, (j - 1) & 1);
@@ -170,21 +161,32 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       alpha_prev = alpha;
-      // write P_j (bf16) in the UMMA SW128 K-major layout: two [128][64] tiles
+      // pass 2: p = exp2(s*scale - max), row sum, P_j (bf16) into the UMMA SW128 K-major layout
+      float rs = 0.f;
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        uint8_t* prow = prow0 + t * TILE;
+      for (int c = 0; c < 4; ++c) {
+        float t[32];
+        tmem_ld32(lane_addr + S_COL + c * 32, t);
+        tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float* x = sv + t * 64 + c * 8;
+        for (int i = 0; i < 32; ++i) {
+          t[i] = (c * 32 + i < kvalid) ? fast_exp2(fmaf(t[i], scale_log2, -mx)) : 0.f;
+          rs += t[i];
+        }
+        uint8_t* prow = prow0 + (c >> 1) * TILE;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int chunk = (c & 1) * 4 + k;  // 16-byte chunk within the 128-byte row
           uint4 u;
-          u.x = pack_bf16(x[0], x[1]);
-          u.y = pack_bf16(x[2], x[3]);
-          u.z = pack_bf16(x[4], x[5]);
-          u.w = pack_bf16(x[6], x[7]);
-          *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) = u;
+          u.x = pack_bf16(t[8 * k + 0], t[8 * k + 1]);
+          u.y = pack_bf16(t[8 * k + 2], t[8 * k + 3]);
+          u.z = pack_bf16(t[8 * k + 4], t[8 * k + 5]);
+          u.w = pack_bf16(t[8 * k + 6], t[8 * k + 7]);
+          *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) = u;
         }
       }
+      l = l * alpha + rs;
+      m_prev = mx;
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(p_full);

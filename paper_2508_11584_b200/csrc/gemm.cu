@@ -1,4 +1,14 @@
 // tcgen05 GEMM engine (see gemm.cuh). sm_100a only.
+//
+// Persistent, warp-specialised: grid = min(tiles, #SMs); each CTA walks tiles t = blockIdx.x,
+// += gridDim.x (M-major over N so co-resident CTAs share the A tile in L2).
+//   warp 0      TMA producer (A: 2D rows or 4D NHWC implicit-conv boxes; B: K-major weights)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-9   epilogue: 2 warps per TMEM lane quadrant, split over 32-column chunks
+// The accumulator is double-buffered in TMEM (2 x BN columns), so tile i's epilogue overlaps
+// tile i+1's mainloop. Row-major bf16/f32 outputs leave through per-warp smem staging and TMA
+// bulk tensor stores (coalesced, OOB-clipped); the fp32 residual update uses TMA reduce-add
+// (cp.reduce.async.bulk .add.f32), so the SM never reads the residual stream.
 #include <cudaTypedefs.h>
 #include <cstdio>
 #include <cstring>
@@ -9,19 +19,22 @@
 
 namespace vpe {
 
-// ------------------------------------------------------------------------------------------
-// device side
-// ------------------------------------------------------------------------------------------
+constexpr int EPI_WARPS = 8;
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int STAGE_BUF = 32 * 32 * 4;  // per epilogue warp: 32 rows x 32 cols x fp32
+
 template <int BN, int BK>
 struct GemmCfg {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 128 ? 4 : 5);
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
-  static constexpr int SWZ_LAYOUT = BK == 64 ? 2 : 4;   // UMMA SWIZZLE_128B / SWIZZLE_64B
-  static constexpr int SBO = 8 * BK * 2;                // bytes between 8-row core groups
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 256;
+  static constexpr int PIPE_BUDGET = 160 * 1024;
+  static constexpr int STAGES_RAW = PIPE_BUDGET / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+  static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : ((2 * BN) <= 64 ? 64 : ((2 * BN) <= 128 ? 128 : ((2 * BN) <= 256 ? 256 : 512)));
+  static constexpr int SWZ_LAYOUT = BK == 64 ? 2 : 4;  // UMMA SWIZZLE_128B / SWIZZLE_64B
+  static constexpr int SBO = 8 * BK * 2;               // bytes between 8-row core groups
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + EPI_WARPS * STAGE_BUF + 256;
 };
 
 VPE_DEV void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32]) {
@@ -57,15 +70,46 @@ VPE_DEV float apply_act(float x, int act) {
   return x;
 }
 
-// Epilogue for one thread: one output row (gpix), 32 consecutive columns starting at col0.
-VPE_DEV void epilogue32(const EpiParams& ep, int64_t gpix, int col0, float (&v)[32]) {
-  const int N = ep.N;
-  const bool full = (col0 + 32 <= N);
-  if (ep.bias) {
+// v[j] += vec[col0 + j] for the valid columns (vectorised when the chunk is full)
+VPE_DEV void add_vec32(float (&v)[32], const float* __restrict__ vec, int col0, int N, bool full) {
+  if (full) {
+    const float4* b4 = reinterpret_cast<const float4*>(vec + col0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 b = __ldg(b4 + i);
+      v[4 * i] += b.x;
+      v[4 * i + 1] += b.y;
+      v[4 * i + 2] += b.z;
+      v[4 * i + 3] += b.w;
+    }
+  } else {
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      if (col0 + j < N) v[j] += __ldg(ep.bias + col0 + j);
+      if (col0 + j < N) v[j] += __ldg(vec + col0 + j);
   }
+}
+VPE_DEV void mul_vec32(float (&v)[32], const float* __restrict__ vec, int col0, int N, bool full) {
+  if (full) {
+    const float4* b4 = reinterpret_cast<const float4*>(vec + col0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 b = __ldg(b4 + i);
+      v[4 * i] *= b.x;
+      v[4 * i + 1] *= b.y;
+      v[4 * i + 2] *= b.z;
+      v[4 * i + 3] *= b.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] *= (col0 + j < N) ? __ldg(vec + col0 + j) : 0.f;
+  }
+}
+
+// Direct (non-TMA) epilogue for one thread: one output row (gpix), 32 consecutive columns.
+VPE_DEV void epilogue_direct(const EpiParams& ep, int64_t gpix, int col0, float (&v)[32]) {
+  const int N = ep.N;
+  const bool full = (col0 + 32 <= N);
+  if (ep.bias) add_vec32(v, ep.bias, col0, N, full);
   switch (ep.kind) {
     case EPI_BF16:
     case EPI_CONV: {
@@ -75,10 +119,12 @@ VPE_DEV void epilogue32(const EpiParams& ep, int64_t gpix, int col0, float (&v)[
           if (ep.add1) load_bf16x32_add(ep.add1 + gpix * ep.ldo + col0, v);
           if (ep.add2) load_bf16x32_add(ep.add2 + gpix * ep.ldo + col0, v);
         } else {
+#pragma unroll
           for (int j = 0; j < 32; ++j) {
-            if (col0 + j >= N) break;
-            if (ep.add1) v[j] += __bfloat162float(ep.add1[gpix * ep.ldo + col0 + j]);
-            if (ep.add2) v[j] += __bfloat162float(ep.add2[gpix * ep.ldo + col0 + j]);
+            if (col0 + j < N) {
+              if (ep.add1) v[j] += __bfloat162float(ep.add1[gpix * ep.ldo + col0 + j]);
+              if (ep.add2) v[j] += __bfloat162float(ep.add2[gpix * ep.ldo + col0 + j]);
+            }
           }
         }
       }
@@ -87,7 +133,9 @@ VPE_DEV void epilogue32(const EpiParams& ep, int64_t gpix, int col0, float (&v)[
       if (full) {
         store_bf16x32(out, v);
       } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) out[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < N) out[j] = __float2bfloat16_rn(v[j]);
       }
       if (ep.out_relu) {
         __nv_bfloat16* o2 = ep.out_relu + gpix * ep.ldo + col0;
@@ -96,50 +144,49 @@ VPE_DEV void epilogue32(const EpiParams& ep, int64_t gpix, int col0, float (&v)[
         if (full) {
           store_bf16x32(o2, v);
         } else {
-          for (int j = 0; j < 32 && col0 + j < N; ++j) o2[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < N) o2[j] = __float2bfloat16_rn(v[j]);
         }
       }
       break;
     }
     case EPI_RESID: {
       float* r = ep.resid + gpix * ep.ldr + col0;
-      if (full) {
-        float4* r4 = reinterpret_cast<float4*>(r);
-        const float4* s4 = reinterpret_cast<const float4*>(ep.scale + col0);
+      mul_vec32(v, ep.scale, col0, N, full);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          float4 h = r4[i], s = __ldg(s4 + i);
-          h.x += s.x * v[4 * i + 0];
-          h.y += s.y * v[4 * i + 1];
-          h.z += s.z * v[4 * i + 2];
-          h.w += s.w * v[4 * i + 3];
-          r4[i] = h;
-        }
-      } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) r[j] += ep.scale[col0 + j] * v[j];
-      }
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < N) r[j] += v[j];
       break;
     }
     case EPI_PATCH: {
       const int64_t img = gpix / ep.rows_per_img;
       const int64_t p = gpix - img * ep.rows_per_img;
       float* r = ep.resid + (gpix + img + 1) * ep.ldr + col0;
-      const float* pos = ep.pos + (p + 1) * (int64_t)N + col0;
-      for (int j = 0; j < 32 && col0 + j < N; ++j) r[j] = v[j] + __ldg(pos + j);
+      add_vec32(v, ep.pos + (p + 1) * (int64_t)N, col0, N, full);
+      if (full) {
+        float4* r4 = reinterpret_cast<float4*>(r);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < N) r[j] = v[j];
+      }
       break;
     }
     case EPI_F32: {
       float* o = reinterpret_cast<float*>(ep.out) + gpix * ep.ldo + col0;
-      if (ep.act != ACT_NONE) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], ep.act);
-      }
+      for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], ep.act);
       if (full) {
         float4* o4 = reinterpret_cast<float4*>(o);
 #pragma unroll
         for (int i = 0; i < 8; ++i) o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = v[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < N) o[j] = v[j];
       }
       break;
     }
@@ -151,13 +198,15 @@ VPE_DEV void epilogue32(const EpiParams& ep, int64_t gpix, int col0, float (&v)[
       const int y = rem / ep.ct_W, x = rem - (rem / ep.ct_W) * ep.ct_W;
       const int k = ep.ct_k, Wo = ep.ct_W * k, Ho = ep.ct_H * k;
       __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ep.out);
+#pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int c = col0 + j;
-        if (c >= N) break;
-        const int s = c / ep.ct_cout, co = c - s * ep.ct_cout;
-        const int ky = s / k, kx = s - ky * k;
-        const int64_t op = (img * Ho + (int64_t)(y * k + ky)) * Wo + (x * k + kx);
-        out[op * ep.ldo + co] = __float2bfloat16_rn(v[j]);
+        if (c < N) {
+          const int s = c / ep.ct_cout, co = c - s * ep.ct_cout;
+          const int ky = s / k, kx = s - ky * k;
+          const int64_t op = (img * Ho + (int64_t)(y * k + ky)) * Wo + (x * k + kx);
+          out[op * ep.ldo + co] = __float2bfloat16_rn(v[j]);
+        }
       }
       break;
     }
@@ -175,28 +224,34 @@ VPE_DEV void epilogue32(const EpiParams& ep, int64_t gpix, int col0, float (&v)[
 }
 
 template <int BN, int BK>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                   const GemmParams p) {
+                   const __grid_constant__ CUtensorMap tout, const GemmParams p) {
   using C = GemmCfg<BN, BK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint8_t* sStage = sB + C::STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + EPI_WARPS * STAGE_BUF);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty + C::STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (warp == 0 && lane == 0) {
     tma_prefetch(&ta);
     tma_prefetch(&tb);
+    if (p.tma_out) tma_prefetch(&tout);
     for (int i = 0; i < C::STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(tfull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], EPI_WARPS * 32);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
@@ -204,81 +259,139 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-
-  const int n0 = blockIdx.x * BN;
-  // tile geometry
-  int m0 = 0, img = 0, y0 = 0, x0 = 0;
-  if (p.mode == 0) {
-    m0 = blockIdx.y * 128;
-  } else {
-    img = blockIdx.y / p.tiles_per_img;
-    const int r = blockIdx.y - img * p.tiles_per_img;
-    y0 = (r / p.tiles_x) * p.bh;
-    x0 = (r % p.tiles_x) * p.bw;
-  }
+  const int ntiles = p.m_tiles * p.n_tiles;
 
   if (warp == 0) {
     if (lane == 0) {
       const int half = p.ks / 2;
-      for (int kb = 0; kb < p.kblocks; ++kb) {
-        const int s = kb % C::STAGES;
-        const uint32_t ph = (kb / C::STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], C::STAGE_BYTES);
-        const int ka = kb % p.kblocks_a;
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+        const int n0 = nt * BN;
+        int m0 = 0, img = 0, y0 = 0, x0 = 0;
         if (p.mode == 0) {
-          tma_load_2d(sA + s * C::A_BYTES, &ta, &full[s], ka * BK, m0);
+          m0 = mt * 128;
         } else {
-          const int tap = ka / p.cchunks, cc = ka - tap * p.cchunks;
-          const int dy = tap / p.ks - half, dx = tap % p.ks - half;
-          tma_load_4d(sA + s * C::A_BYTES, &ta, &full[s], cc * BK, x0 + dx, y0 + dy, img);
+          img = mt / p.tiles_per_img;
+          const int r = mt - img * p.tiles_per_img;
+          y0 = (r / p.tiles_x) * p.bh;
+          x0 = (r % p.tiles_x) * p.bw;
         }
-        tma_load_2d(sB + s * C::B_BYTES, &tb, &full[s], kb * BK, n0);
+        for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          const uint32_t ph = (it / C::STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], C::STAGE_BYTES);
+          const int ka = kb % p.kblocks_a;
+          if (p.mode == 0) {
+            tma_load_2d(sA + s * C::A_BYTES, &ta, &full[s], ka * BK, m0);
+          } else {
+            const int tap = ka / p.cchunks, cc = ka - tap * p.cchunks;
+            const int dy = tap / p.ks - half, dx = tap % p.ks - half;
+            tma_load_4d(sA + s * C::A_BYTES, &ta, &full[s], cc * BK, x0 + dx, y0 + dy, img);
+          }
+          tma_load_2d(sB + s * C::B_BYTES, &tb, &full[s], kb * BK, n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(128, BN);
-      for (int kb = 0; kb < p.kblocks; ++kb) {
-        const int s = kb % C::STAGES;
-        const uint32_t ph = (kb / C::STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA + s * C::A_BYTES);
-        const uint32_t b0 = smem_u32(sB + s * C::B_BYTES);
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          const uint32_t ph = (it / C::STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          const uint64_t ad = smem_desc(a0 + k * 32, 16, C::SBO, C::SWZ_LAYOUT);
-          const uint64_t bd = smem_desc(b0 + k * 32, 16, C::SBO, C::SWZ_LAYOUT);
-          umma_f16(tmem, ad, bd, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = smem_desc(a0 + k * 32, 16, C::SBO, C::SWZ_LAYOUT);
+            const uint64_t bd = smem_desc(b0 + k * 32, 16, C::SBO, C::SWZ_LAYOUT);
+            umma_f16(d, ad, bd, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&tfull[acc]);
       }
-      umma_commit(tfull);
     }
   } else {
-    // epilogue: warps 2..5 -> TMEM lane quadrant (warp % 4)
-    mbar_wait(tfull, 0);
-    tc_fence_after();
+    // epilogue warps 2..9: TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4
+    const int e = warp - 2;
     const int q = warp & 3;
+    const int chalf = e >> 2;
     const int r = q * 32 + lane;
-    int64_t gpix;
-    bool valid;
-    if (p.mode == 0) {
-      gpix = m0 + r;
-      valid = gpix < p.M;
-    } else {
-      const int y = y0 + r / p.bw, x = x0 + r % p.bw;
-      valid = (y < p.H) && (x < p.W);
-      gpix = ((int64_t)img * p.H + y) * p.W + x;
-    }
+    uint8_t* stg = sStage + e * STAGE_BUF;
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int acc = i & 1;
+      const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+      const int n0 = nt * BN;
+      int64_t gpix;
+      bool valid;
+      int m0 = 0;
+      if (p.mode == 0) {
+        m0 = mt * 128;
+        gpix = m0 + r;
+        valid = gpix < p.M;
+      } else {
+        const int img = mt / p.tiles_per_img;
+        const int rr = mt - img * p.tiles_per_img;
+        const int y = (rr / p.tiles_x) * p.bh + r / p.bw, x = (rr % p.tiles_x) * p.bw + r % p.bw;
+        valid = (y < p.H) && (x < p.W);
+        gpix = ((int64_t)img * p.H + y) * p.W + x;
+      }
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      tc_fence_after();
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c0, v);
-      tmem_ld_wait();
-      if (valid && n0 + c0 < p.ep.N) epilogue32(p.ep, gpix, n0 + c0, v);
+      for (int c = chalf; c < BN / 32; c += 2) {
+        const int c0 = c * 32;
+        float v[32];
+        tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c0, v);
+        tmem_ld_wait();
+        const int col0 = n0 + c0;
+        if (col0 >= p.ep.N) continue;  // warp-uniform
+        if (p.tma_out) {
+          const int N = p.ep.N;
+          const bool fullc = col0 + 32 <= N;
+          if (p.ep.bias) add_vec32(v, p.ep.bias, col0, N, fullc);
+          if (p.ep.kind == EPI_RESID) mul_vec32(v, p.ep.scale, col0, N, fullc);
+          if (p.ep.act != ACT_NONE) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], p.ep.act);
+          }
+          if (lane == 0) bulk_wait_read0();  // staging buffer free again
+          __syncwarp();
+          if (p.ep.kind == EPI_BF16) {
+            store_bf16x32(reinterpret_cast<__nv_bfloat16*>(stg + lane * 64), v);
+          } else {
+            float4* s4 = reinterpret_cast<float4*>(stg + lane * 128);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (p.ep.kind == EPI_RESID)
+              tma_reduce_add_2d(&tout, stg, col0, m0 + q * 32);
+            else
+              tma_store_2d(&tout, stg, col0, m0 + q * 32);
+            bulk_commit();
+          }
+        } else if (valid) {
+          epilogue_direct(p.ep, gpix, col0, v);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -292,6 +405,7 @@ __global__ void __launch_bounds__(192, 1)
 // host side
 // ------------------------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static int g_num_sms = 0;
 
 bool tma_available() {
   if (g_encode) return true;
@@ -304,12 +418,22 @@ bool tma_available() {
   return true;
 }
 
-int encode_tma(CUtensorMap* m, int rank, const void* ptr, const uint64_t* dims, const uint64_t* strides_bytes,
-                  const uint32_t* box, CUtensorMapSwizzle swz) {
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+int encode_tma_t(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* ptr, const uint64_t* dims,
+                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz) {
   if (!tma_available()) return VPE_E_CUDA;
   uint32_t es[5] = {1, 1, 1, 1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides_bytes, box,
-                        es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = g_encode(m, dt, rank, const_cast<void*>(ptr), dims, strides_bytes, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     fprintf(stderr, "[vpe] cuTensorMapEncodeTiled failed (%d) rank=%d dims=%llu,%llu box=%u,%u\n", (int)r, rank,
@@ -317,6 +441,11 @@ int encode_tma(CUtensorMap* m, int rank, const void* ptr, const uint64_t* dims, 
     return VPE_E_SHAPE;
   }
   return VPE_OK;
+}
+
+int encode_tma(CUtensorMap* m, int rank, const void* ptr, const uint64_t* dims, const uint64_t* strides_bytes,
+               const uint32_t* box, CUtensorMapSwizzle swz) {
+  return encode_tma_t(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, ptr, dims, strides_bytes, box, swz);
 }
 
 static int smem_for(int bn, int bk) {
@@ -333,6 +462,33 @@ static int make_b_map(GemmPlan* g, const __nv_bfloat16* B, int N, int Kb, int64_
   uint64_t strides[1] = {(uint64_t)ldb * 2};
   uint32_t box[2] = {(uint32_t)bk, (uint32_t)bn};
   return encode_tma(&g->tb, 2, B, dims, strides, box, bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+// TMA-store epilogue for row-major outputs (bf16 / f32 store, f32 residual reduce-add)
+static int make_out_map(GemmPlan* g, int M) {
+  const EpiParams& ep = g->p.ep;
+  if (ep.kind != EPI_BF16 && ep.kind != EPI_F32 && ep.kind != EPI_RESID) return VPE_OK;
+  if (ep.out_relu) return VPE_OK;
+  const bool bf = ep.kind == EPI_BF16;
+  void* base = ep.kind == EPI_RESID ? static_cast<void*>(ep.resid) : ep.out;
+  const int64_t ld = ep.kind == EPI_RESID ? ep.ldr : ep.ldo;
+  const int esz = bf ? 2 : 4;
+  if ((ld * esz) % 16 || reinterpret_cast<uintptr_t>(base) % 16 || ep.N % (16 / esz)) return VPE_OK;
+  uint64_t dims[2] = {(uint64_t)ep.N, (uint64_t)M};
+  uint64_t strides[1] = {(uint64_t)ld * esz};
+  uint32_t box[2] = {32u, 32u};
+  VPE_TRY(encode_tma_t(&g->tout, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
+                       strides, box, CU_TENSOR_MAP_SWIZZLE_NONE));
+  g->p.tma_out = 1;
+  return VPE_OK;
+}
+
+static void finish_grid(GemmPlan* g, int N, int bn, int m_tiles) {
+  g->p.n_tiles = (N + bn - 1) / bn;
+  g->p.m_tiles = m_tiles;
+  const int tiles = g->p.n_tiles * m_tiles;
+  const int ctas = tiles < num_sms() ? tiles : num_sms();
+  g->grid = dim3(ctas, 1, 1);
 }
 
 int plan_gemm_rows(GemmPlan* g, const __nv_bfloat16* A, int M, int K, int64_t lda, const __nv_bfloat16* B, int N,
@@ -354,7 +510,8 @@ int plan_gemm_rows(GemmPlan* g, const __nv_bfloat16* A, int M, int K, int64_t ld
   g->p.ks = 1;
   g->p.cchunks = 1;
   g->p.ep = ep;
-  g->grid = dim3((N + bn - 1) / bn, (M + 127) / 128, 1);
+  if ((rc = make_out_map(g, M))) return rc;
+  finish_grid(g, N, bn, (M + 127) / 128);
   g->bn = bn;
   g->bk = bk;
   g->smem = smem_for(bn, bk);
@@ -371,7 +528,7 @@ int plan_gemm_conv(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   if ((pitch_px * 2) % 16 || (pitch_row * 2) % 16 || (pitch_img * 2) % 16 || reinterpret_cast<uintptr_t>(X) % 16)
     return VPE_E_SHAPE;
   memset(g, 0, sizeof(*g));
-  // spatial tile bw x bh = 128 pixels; pick bw (power of two <= 128) minimising padded width
+  // spatial tile bw x bh = 128 pixels; pick bw (power of two <= 128) minimising padded area
   int best_bw = 128, best_cost = 1 << 30;
   for (int bw = 128; bw >= 1; bw >>= 1) {
     const int bh = 128 / bw;
@@ -401,7 +558,7 @@ int plan_gemm_conv(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   g->p.tiles_per_img = g->p.tiles_x * ((H + bh - 1) / bh);
   g->p.M = nimg * H * W;
   g->p.ep = ep;
-  g->grid = dim3((N + bn - 1) / bn, nimg * g->p.tiles_per_img, 1);
+  finish_grid(g, N, bn, nimg * g->p.tiles_per_img);
   g->bn = bn;
   g->bk = bk;
   g->smem = smem_for(bn, bk);
@@ -416,7 +573,7 @@ static int launch_t(const GemmPlan& g, cudaStream_t s) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GemmCfg<BN, BK>::SMEM);
     attr_set = true;
   }
-  k<<<g.grid, 192, GemmCfg<BN, BK>::SMEM, s>>>(g.ta, g.tb, g.p);
+  k<<<g.grid, GEMM_THREADS, GemmCfg<BN, BK>::SMEM, s>>>(g.ta, g.tb, g.tout, g.p);
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
 }
 

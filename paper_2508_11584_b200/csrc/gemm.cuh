@@ -54,12 +54,15 @@ struct GemmParams {
   int ks = 1;          // conv kernel size
   int cchunks = 1;     // channel chunks (of BK) per tap
   int H = 0, W = 0, bw = 0, bh = 0, tiles_x = 0, tiles_per_img = 0;
+  int m_tiles = 0, n_tiles = 0;  // persistent tile space
+  int tma_out = 0;               // 1: epilogue leaves through TMA store / reduce-add (tout)
   EpiParams ep;
 };
 
 struct GemmPlan {
   CUtensorMap ta;
   CUtensorMap tb;
+  CUtensorMap tout;
   GemmParams p;
   dim3 grid;
   int bn = 0, bk = 0;

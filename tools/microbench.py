@@ -1,0 +1,56 @@
+"""Kernel microbenchmarks (CUDA events on the launching stream): GEMM variants, attention, LN."""
+import argparse
+import json
+import sys
+import os
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_2508_11584_b200 import _ops
+
+
+def timeit(fn, reps=100, warm=10):
+    for _ in range(warm):
+        fn()
+    s = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(s)
+    for _ in range(reps):
+        fn()
+    b.record(s)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps * 1e3  # us
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--only", default="")
+    args = p.parse_args()
+    dev = torch.device("cuda")
+    res = []
+    for (M, N, K) in [(16400, 1536, 384), (16400, 384, 1536), (16400, 1152, 384), (8192, 8192, 8192)]:
+        a = torch.randn(M, K, device=dev).to(torch.bfloat16)
+        w = (torch.randn(N, K, device=dev) * 0.02).to(torch.bfloat16)
+        bias = torch.zeros(N, device=dev)
+        out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        outf = torch.empty(M, N, device=dev, dtype=torch.float32)
+        for bn in (64, 128, 256):
+            for act in (0, 1):
+                us = timeit(lambda: _ops.linear(a, w, bias=bias, out=out, act=act, bn=bn))
+                tf = 2 * M * N * K / us * 1e-6
+                res.append(dict(M=M, N=N, K=K, bn=bn, act=act, us=us, tflops=tf))
+                print(json.dumps(res[-1]), flush=True)
+        us = timeit(lambda: torch.matmul(a, w.t(), out=out))
+        print(json.dumps(dict(M=M, N=N, K=K, impl="cublas", us=us, tflops=2 * M * N * K / us * 1e-6)), flush=True)
+    for (B, T, H) in [(16, 1025, 6), (1, 1025, 6)]:
+        D = H * 64
+        qkv = torch.randn(B * T, 3 * D, device=dev).to(torch.bfloat16)
+        us = timeit(lambda: _ops.attention(qkv, B, T, D, H))
+        fl = 4.0 * B * T * T * D
+        print(json.dumps(dict(kernel="attention", B=B, T=T, H=H, us=us, tflops=fl / us * 1e-6)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
