@@ -215,6 +215,7 @@ def run_ours(args):
     from paper_2508_11584_b200 import _lib
     from paper_2508_11584_b200.config import model_config
     from paper_2508_11584_b200.engine import VPEngine
+    from paper_2508_11584_b200.sharding import max_over_ranks, streams_for_rank
     from paper_2508_11584_b200.weights import make_frames, make_weights
 
     cfg = model_config(args.model)
@@ -224,7 +225,9 @@ def run_ours(args):
     # input pool larger than L2, cycled: distinct frames every step (camera stream ids sharded by rank)
     frame_bytes = B * 3 * R * R
     npool = max(4, (2 * L2_BYTES) // frame_bytes + 1)
-    base = make_frames(B, R, stream_id=rank)
+    # this rank's camera streams (stream i -> GPU i mod world); each contributes batch-1 frames
+    my_streams = streams_for_rank(B * world, rank, world)
+    base = torch.cat([make_frames(1, R, stream_id=s) for s in my_streams], 0)
     pool_dev = torch.empty(npool, B, 3, R, R, dtype=torch.uint8, device=eng.device)
     for i in range(npool):
         pool_dev[i].copy_(torch.roll(base, shifts=i * 7, dims=-1))
@@ -262,10 +265,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         dt = ev0.elapsed_time(ev1) * 1e-3
         launches = _lib.lib.vpe_kernel_launches() - launches0
-        if dist:
-            t = torch.tensor([dt], device=eng.device, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = max_over_ranks(dt, dist, eng.device)
         return dt, launches
 
     with ClockSampler(local) as clk:

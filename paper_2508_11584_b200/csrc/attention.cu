@@ -15,7 +15,9 @@ namespace vpe {
 
 namespace {
 constexpr int TILE = 16 * 1024;  // one [128][64] bf16 SW128 tile
-constexpr int SMEM_ATT = 1024 + TILE /*Q*/ + 2 * TILE /*K*/ + 2 * TILE /*V*/ + 2 * TILE /*P*/ + 256;
+// Q + K double-buffered + V single-buffered + P: 96 KB -> two CTAs per SM, so one CTA's
+// softmax overlaps the other's tensor-core work (ncu: 1 CTA/SM left the tensor pipe 88% idle)
+constexpr int SMEM_ATT = 1024 + TILE /*Q*/ + 2 * TILE /*K*/ + TILE /*V*/ + 2 * TILE /*P*/ + 256;
 constexpr int S_COL = 0, O_COL = 128, TMEM_COLS = 256;
 }  // namespace
 
@@ -27,12 +29,13 @@ __global__ void __launch_bounds__(192, 2)
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + TILE;
   uint8_t* sV = sK + 2 * TILE;
-  uint8_t* sP = sV + 2 * TILE;
+  uint8_t* sP = sV + TILE;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * TILE);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* v_full = bars + 3;   // [2]
-  uint64_t* kv_empty = bars + 5; // [2]
+  uint64_t* k_empty = bars + 3;  // [2] freed when S_j completes
+  uint64_t* v_full = bars + 5;
+  uint64_t* v_empty = bars + 6;  // freed when PV_j completes
   uint64_t* s_full = bars + 7;
   uint64_t* p_full = bars + 8;
   uint64_t* o_full = bars + 9;
@@ -49,9 +52,10 @@ __global__ void __launch_bounds__(192, 2)
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_empty[i], 1);
     }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
     mbar_init(s_full, 1);
     mbar_init(p_full, 128);
     mbar_init(o_full, 1);
@@ -67,13 +71,19 @@ __global__ void __launch_bounds__(192, 2)
     if (lane == 0) {
       mbar_expect_tx(q_full, TILE);
       tma_load_2d(sQ, &tqkv, q_full, head * 64, row_base + q0);
+      mbar_expect_tx(&k_full[0], TILE);
+      tma_load_2d(sK, &tqkv, &k_full[0], D + head * 64, row_base);
+      // order K_{j+1} before V_j: K_{j+1} only waits for S_{j-1}, V_j waits for PV_{j-1}
       for (int j = 0; j < nkv; ++j) {
-        const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&k_full[s], TILE);
-        tma_load_2d(sK + s * TILE, &tqkv, &k_full[s], D + head * 64, row_base + j * 128);
-        mbar_expect_tx(&v_full[s], TILE);
-        tma_load_2d(sV + s * TILE, &tqkv, &v_full[s], 2 * D + head * 64, row_base + j * 128);
+        if (j + 1 < nkv) {
+          const int s = (j + 1) & 1;
+          mbar_wait(&k_empty[s], (((j + 1) >> 1) & 1) ^ 1);
+          mbar_expect_tx(&k_full[s], TILE);
+          tma_load_2d(sK + s * TILE, &tqkv, &k_full[s], D + head * 64, row_base + (j + 1) * 128);
+        }
+        mbar_wait(v_empty, (j & 1) ^ 1);
+        mbar_expect_tx(v_full, TILE);
+        tma_load_2d(sV, &tqkv, v_full, 2 * D + head * 64, row_base + j * 128);
       }
     }
   } else if (warp == 1) {
@@ -91,6 +101,7 @@ __global__ void __launch_bounds__(192, 2)
           umma_f16(tmem + S_COL, smem_desc(q_addr + k * 32, 16, 1024, 2), smem_desc(k_addr + k * 32, 16, 1024, 2),
                    idesc_s, k > 0);
         umma_commit(s_full);
+        umma_commit(&k_empty[0]);
       }
       for (int j = 0; j < nkv; ++j) {
         mbar_wait(p_full, j & 1);
@@ -105,11 +116,11 @@ __global__ void __launch_bounds__(192, 2)
             umma_f16(tmem + S_COL, smem_desc(q_addr + k * 32, 16, 1024, 2), smem_desc(k_addr + k * 32, 16, 1024, 2),
                      idesc_s, k > 0);
           umma_commit(s_full);
+          umma_commit(&k_empty[s1]);
         }
-        const int s = j & 1;
-        mbar_wait(&v_full[s], (j >> 1) & 1);
+        mbar_wait(v_full, j & 1);
         tc_fence_after();
-        const uint32_t v_addr = smem_u32(sV + s * TILE);
+        const uint32_t v_addr = smem_u32(sV);
         const uint32_t p_addr = smem_u32(sP);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -118,7 +129,7 @@ __global__ void __launch_bounds__(192, 2)
                    k > 0);
         }
         umma_commit(o_full);
-        umma_commit(&kv_empty[s]);
+        umma_commit(v_empty);
       }
     }
   } else {

@@ -103,8 +103,12 @@ int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32
   const int kb = ks * ks * Cp;
   const int bn = N <= 32 ? 32 : (N <= 64 ? 64 : 128);
   GemmPlan g;
-  VPE_TRY(plan_gemm_conv(&g, static_cast<const __nv_bfloat16*>(x), B, H, W, C, Cp, (int64_t)W * Cp,
-                         (int64_t)H * W * Cp, ks, bk, static_cast<const __nv_bfloat16*>(w), N, kb, kb, ep, bn));
+  const bool halo = ks == 3 && plan_conv_halo(&g, static_cast<const __nv_bfloat16*>(x), B, H, W, Cp, Cp,
+                                              (int64_t)W * Cp, (int64_t)H * W * Cp, 1,
+                                              static_cast<const __nv_bfloat16*>(w), N, kb, ep, bn) == VPE_OK;
+  if (!halo)
+    VPE_TRY(plan_gemm_conv(&g, static_cast<const __nv_bfloat16*>(x), B, H, W, C, Cp, (int64_t)W * Cp,
+                           (int64_t)H * W * Cp, ks, bk, static_cast<const __nv_bfloat16*>(w), N, kb, kb, ep, bn));
   VPE_TRY(launch_gemm(g, static_cast<cudaStream_t>(stream)));
   count_launches(1);
   return VPE_OK;

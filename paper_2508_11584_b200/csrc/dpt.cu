@@ -44,6 +44,9 @@ struct vpe_dpt {
 
 static int conv_plan(GemmPlan* g, const bf16* x, int B, int S, int Cp, const void* w, int N, const EpiParams& ep) {
   const int kb = 9 * Cp;
+  if (plan_conv_halo(g, x, B, S, S, Cp, Cp, (int64_t)S * Cp, (int64_t)S * S * Cp, 1, static_cast<const bf16*>(w), N,
+                     kb, ep, bn_for(N)) == VPE_OK)
+    return VPE_OK;
   return plan_gemm_conv(g, x, B, S, S, Cp, Cp, (int64_t)S * Cp, (int64_t)S * S * Cp, 3, bk_for(Cp),
                         static_cast<const bf16*>(w), N, kb, kb, ep, bn_for(N));
 }

@@ -402,6 +402,173 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// 3x3 convolution with a shared halo tile (mode 2).
+//
+// The 4D-box implicit GEMM above re-reads the input once per tap (9x the L2->SMEM traffic).
+// Here one TMA (5D map {8ch, x, y, chunk, img}) brings the (rows+2) x P halo of a 128-pixel
+// output tile for a whole channel group into SMEM in the UMMA no-swizzle K-major layout
+// ("core matrix" = 8 pixels x 16 B, pixels 16 B apart, 8-channel chunks LBO apart). Every tap
+// is then just a different descriptor start address: + (dy*P + dx) * 16 B. Output pixels are
+// "virtual" positions v = ry*P + rx of the padded row pitch P; the 2 halo columns per row are
+// computed and discarded by the epilogue.
+// ------------------------------------------------------------------------------------------
+template <int BN, int KC>
+struct HaloCfg {
+  static constexpr int GCH = 8 * KC;                 // channels per group
+  static constexpr int A_MAX = KC * 130 * 3 * 16;    // largest halo stage (P=130, 3 rows)
+  static constexpr int A_STAGES = 2;
+  static constexpr int B_BYTES = BN * GCH * 2;       // one tap's weight tile
+  static constexpr int B_STAGES = BN >= 128 ? 4 : 8;
+  static constexpr int TMEM_COLS = GemmCfg<BN, 64>::TMEM_COLS;
+  static constexpr int B_SWZ = GCH == 64 ? 2 : 4;
+  static constexpr int B_SBO = 8 * GCH * 2;
+  static constexpr size_t SMEM = 1024 + (size_t)A_STAGES * A_MAX + (size_t)B_STAGES * B_BYTES + 256;
+};
+
+template <int BN, int KC>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    conv_halo_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                     const GemmParams p) {
+  using C = HaloCfg<BN, KC>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = smem;  // 1024-aligned for the swizzled weight tiles
+  uint8_t* sA = sB + C::B_STAGES * C::B_BYTES;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sA + C::A_STAGES * C::A_MAX);
+  uint64_t* a_empty = a_full + C::A_STAGES;
+  uint64_t* b_full = a_empty + C::A_STAGES;
+  uint64_t* b_empty = b_full + C::B_STAGES;
+  uint64_t* tfull = b_empty + C::B_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int P = p.hp, rows_box = p.rows_box;
+  const int a_bytes = KC * P * rows_box * 16;
+  const int chunk_stride = P * rows_box * 16;  // LBO: distance between 8-channel chunks
+  const int nb = p.parts * 9;                  // weight tiles per halo stage
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&ta);
+    tma_prefetch(&tb);
+    for (int i = 0; i < C::A_STAGES; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < C::B_STAGES; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], EPI_WARPS * 32);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int ntiles = p.m_tiles * p.n_tiles;
+  const int groups = p.cchunks;  // channel groups of GCH
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int ia = 0, ib = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+        const int img = mt / p.tiles_per_img, rr = mt - img * p.tiles_per_img;
+        const int y0 = (rr / p.tiles_x) * p.bh, x0 = (rr % p.tiles_x) * p.bw;
+        for (int g = 0; g < groups; ++g, ++ia) {
+          const int sa = ia % C::A_STAGES;
+          mbar_wait(&a_empty[sa], ((ia / C::A_STAGES) & 1) ^ 1);
+          mbar_expect_tx(&a_full[sa], a_bytes);
+          tma_load_5d(sA + sa * C::A_MAX, &ta, &a_full[sa], 0, x0 - 1, y0 - 1, g * KC, img);
+          for (int j = 0; j < nb; ++j, ++ib) {
+            const int sb = ib % C::B_STAGES;
+            mbar_wait(&b_empty[sb], ((ib / C::B_STAGES) & 1) ^ 1);
+            mbar_expect_tx(&b_full[sb], C::B_BYTES);
+            const int part = j / 9, tap = j - part * 9;
+            tma_load_2d(sB + sb * C::B_BYTES, &tb, &b_full[sb], (part * 9 + tap) * p.kcp + g * C::GCH, nt * BN);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN);
+      int ia = 0, ib = 0, i = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        bool first = true;
+        for (int g = 0; g < groups; ++g, ++ia) {
+          const int sa = ia % C::A_STAGES;
+          mbar_wait(&a_full[sa], (ia / C::A_STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + sa * C::A_MAX);
+          for (int j = 0; j < nb; ++j, ++ib) {
+            const int sb = ib % C::B_STAGES;
+            mbar_wait(&b_full[sb], (ib / C::B_STAGES) & 1);
+            tc_fence_after();
+            const int tap = j % 9;
+            const int dy = tap / 3, dx = tap - (tap / 3) * 3;
+            const uint32_t at = a0 + (uint32_t)((dy * P + dx) * 16);
+            const uint32_t b0 = smem_u32(sB + sb * C::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < KC / 2; ++k) {
+              const uint64_t ad = smem_desc(at + 2 * k * chunk_stride, chunk_stride, 128, 0);
+              const uint64_t bd = smem_desc(b0 + k * 32, 16, C::B_SBO, C::B_SWZ);
+              umma_f16(d, ad, bd, idesc, first ? 0u : 1u);
+              first = false;
+            }
+            umma_commit(&b_empty[sb]);
+          }
+          umma_commit(&a_empty[sa]);
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    const int e = warp - 2;
+    const int q = warp & 3;
+    const int chalf = e >> 2;
+    const int r = q * 32 + lane;  // virtual output position within the tile
+    const int ry = r / P, rx = r - (r / P) * P;
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int acc = i & 1;
+      const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+      const int img = mt / p.tiles_per_img, rr = mt - img * p.tiles_per_img;
+      const int y = (rr / p.tiles_x) * p.bh + ry, x = (rr % p.tiles_x) * p.bw + rx;
+      const bool valid = ry < p.bh && rx < p.bw && y < p.H && x < p.W;
+      const int64_t gpix = ((int64_t)img * p.H + y) * p.W + x;
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = chalf; c < BN / 32; c += 2) {
+        const int c0 = c * 32;
+        float v[32];
+        tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c0, v);
+        tmem_ld_wait();
+        const int col0 = nt * BN + c0;
+        if (valid && col0 < p.ep.N) epilogue_direct(p.ep, gpix, col0, v);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -565,6 +732,77 @@ int plan_gemm_conv(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   return VPE_OK;
 }
 
+int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, int Cp, int64_t pitch_px,
+                   int64_t pitch_row, int64_t pitch_img, int parts, const __nv_bfloat16* B, int N, int64_t ldb,
+                   const EpiParams& ep, int bn) {
+  if (Cp % 32 || (bn != 32 && bn != 64 && bn != 128)) return VPE_E_SHAPE;
+  const int kc = (Cp % 64 == 0) ? 8 : 4;
+  if (Cp == 32) {
+    if (kc != 4) return VPE_E_SHAPE;
+  } else if (Cp % 64) {
+    return VPE_E_SHAPE;
+  }
+  int bw, P, rows;
+  if (W >= 128) {
+    bw = 128;
+    P = 130;
+    rows = 1;
+  } else {
+    bw = W;
+    P = W + 2;
+    rows = 128 / P;
+  }
+  if (rows < 1 || (double)(rows * bw) / 128.0 < 0.7) return VPE_E_SHAPE;
+  const int rows_box = 129 / P + 3;
+  if (P > 256 || rows_box > 256) return VPE_E_SHAPE;
+  if ((pitch_px * 2) % 16 || (pitch_row * 2) % 16 || (pitch_img * 2) % 16 || reinterpret_cast<uintptr_t>(X) % 16)
+    return VPE_E_SHAPE;
+  memset(g, 0, sizeof(*g));
+  // 5D view {8 ch, x, y, chunk, img}: TMA writes [chunk][y][x][8ch] = the no-swizzle K-major layout
+  uint64_t dims[5] = {8, (uint64_t)W, (uint64_t)H, (uint64_t)(Cp / 8), (uint64_t)nimg};
+  uint64_t strides[4] = {(uint64_t)pitch_px * 2, (uint64_t)pitch_row * 2, 16, (uint64_t)pitch_img * 2};
+  uint32_t box[5] = {8u, (uint32_t)P, (uint32_t)rows_box, (uint32_t)kc, 1u};
+  VPE_TRY(encode_tma(&g->ta, 5, X, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE));
+  const int gch = 8 * kc;
+  VPE_TRY(make_b_map(g, B, N, parts * 9 * Cp, ldb, bn, gch));
+  g->p.mode = 2;
+  g->p.hp = P;
+  g->p.rows_box = rows_box;
+  g->p.parts = parts;
+  g->p.kcp = Cp;
+  g->p.cchunks = Cp / gch;  // channel groups
+  g->p.ks = 3;
+  g->p.H = H;
+  g->p.W = W;
+  g->p.bw = bw;
+  g->p.bh = rows;
+  g->p.tiles_x = (W + bw - 1) / bw;
+  g->p.tiles_per_img = g->p.tiles_x * ((H + rows - 1) / rows);
+  g->p.M = nimg * H * W;
+  g->p.ep = ep;
+  finish_grid(g, N, bn, nimg * g->p.tiles_per_img);
+  g->bn = bn;
+  g->bk = gch;
+  g->halo_kc = kc;
+#define VPE_HS(BN_, KC_) \
+  if (bn == BN_ && kc == KC_) g->smem = HaloCfg<BN_, KC_>::SMEM;
+  VPE_HS(32, 4) VPE_HS(64, 4) VPE_HS(128, 4) VPE_HS(32, 8) VPE_HS(64, 8) VPE_HS(128, 8)
+#undef VPE_HS
+  return VPE_OK;
+}
+
+template <int BN, int KC>
+static int launch_halo_t(const GemmPlan& g, cudaStream_t s) {
+  auto k = conv_halo_kernel<BN, KC>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg<BN, KC>::SMEM);
+    attr_set = true;
+  }
+  k<<<g.grid, GEMM_THREADS, HaloCfg<BN, KC>::SMEM, s>>>(g.ta, g.tb, g.p);
+  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+}
+
 template <int BN, int BK>
 static int launch_t(const GemmPlan& g, cudaStream_t s) {
   auto k = gemm_tc_kernel<BN, BK>;
@@ -578,6 +816,13 @@ static int launch_t(const GemmPlan& g, cudaStream_t s) {
 }
 
 int launch_gemm(const GemmPlan& g, cudaStream_t s) {
+  if (g.halo_kc) {
+#define VPE_LH(BN_, KC_) \
+  if (g.bn == BN_ && g.halo_kc == KC_) return launch_halo_t<BN_, KC_>(g, s);
+    VPE_LH(32, 4) VPE_LH(64, 4) VPE_LH(128, 4) VPE_LH(32, 8) VPE_LH(64, 8) VPE_LH(128, 8)
+#undef VPE_LH
+    return VPE_E_SHAPE;
+  }
 #define VPE_L(BN_, BK_) \
   if (g.bn == BN_ && g.bk == BK_) return launch_t<BN_, BK_>(g, s);
   VPE_L(32, 64) VPE_L(64, 64) VPE_L(128, 64) VPE_L(256, 64) VPE_L(32, 32) VPE_L(64, 32)

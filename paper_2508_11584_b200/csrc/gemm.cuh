@@ -56,6 +56,8 @@ struct GemmParams {
   int H = 0, W = 0, bw = 0, bh = 0, tiles_x = 0, tiles_per_img = 0;
   int m_tiles = 0, n_tiles = 0;  // persistent tile space
   int tma_out = 0;               // 1: epilogue leaves through TMA store / reduce-add (tout)
+  int hp = 0, rows_box = 0;      // halo conv: virtual row pitch P, halo rows per stage
+  int parts = 1, kcp = 0;        // halo conv: split-precision weight parts, K extent per tap (Cpad)
   EpiParams ep;
 };
 
@@ -66,8 +68,17 @@ struct GemmPlan {
   GemmParams p;
   dim3 grid;
   int bn = 0, bk = 0;
+  int halo_kc = 0;  // > 0: conv_halo_kernel<bn, halo_kc>
   size_t smem = 0;
 };
+
+// 3x3 / stride 1 / pad 1 conv with a shared halo tile (see gemm.cu). X: NHWC with Cp channels
+// (multiple of 32), pitches in elements; weights [N, parts*9*Cp] tap-major. Returns VPE_E_SHAPE
+// when the halo tiling would waste too much of the 128-row MMA (caller falls back to
+// plan_gemm_conv).
+int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, int Cp, int64_t pitch_px,
+                   int64_t pitch_row, int64_t pitch_img, int parts, const __nv_bfloat16* B, int N, int64_t ldb,
+                   const EpiParams& ep, int bn);
 
 // --- host-side builders (gemm.cu) ---
 bool tma_available();

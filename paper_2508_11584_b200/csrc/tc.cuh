@@ -76,6 +76,15 @@ VPE_DEV void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c
       : "memory");
 }
 
+VPE_DEV void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2, int c3,
+                         int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+
 // smem -> global tensor store / reduce-add (bulk async group, issued by one thread)
 VPE_DEV void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -167,7 +176,23 @@ VPE_DEV float fast_exp2(float x) {
   return y;
 }
 
-VPE_DEV float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+// exact-erf GELU (transformers activations.py:70-89), erf via Abramowitz-Stegun 7.1.26
+// (|error| <= 1.5e-7, below the bf16 output rounding): one MUFU rcp + one MUFU ex2 + 8 FMA,
+// versus libdevice erff's branchy two-range polynomial.
+VPE_DEV float gelu_erf(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  float t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  p *= t;
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
+  const float y = fmaf(-p, e, 1.0f);  // erf(|x|/sqrt2)
+  return 0.5f * x * (1.0f + copysignf(y, x));
+}
 
 VPE_DEV uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);

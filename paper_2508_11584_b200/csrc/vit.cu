@@ -30,9 +30,13 @@ struct vpe_vit {
 
 static constexpr int KPATCH = 640;
 
+// BN per GEMM: wide tiles amortise the A re-read; at small M fall back to narrower tiles so
+// the persistent grid still covers the SMs (microbench, profiles/round1_gemm.md).
 static int pick_bn(int N, int M) {
-  (void)M;
-  return N <= 512 ? 64 : 128;
+  const int m_tiles = (M + 127) / 128;
+  int bn = 128;
+  while (bn > 64 && m_tiles * ((N + bn - 1) / bn) < 148) bn >>= 1;
+  return bn;
 }
 
 extern "C" int vpe_vit_create(const vpe_vit_config* cfg, const vpe_vit_weights* w, vpe_vit** out) {

@@ -27,6 +27,7 @@ def timeit(fn, reps=100, warm=10):
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--only", default="")
+    p.add_argument("--conv", action="store_true")
     args = p.parse_args()
     dev = torch.device("cuda")
     res = []
@@ -54,3 +55,19 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def conv_bench():
+    dev = torch.device("cuda")
+    for (B, H, C, N) in [(16, 128, 64, 64), (16, 256, 64, 32), (16, 448, 32, 32), (16, 64, 64, 64), (16, 32, 384, 384)]:
+        x = torch.randn(B, H, H, C, device=dev).to(torch.bfloat16)
+        w = (torch.randn(N, 9 * C, device=dev) * 0.02).to(torch.bfloat16)
+        bias = torch.zeros(N, device=dev)
+        out = torch.empty(B, H, H, N, device=dev, dtype=torch.bfloat16)
+        us = timeit(lambda: _ops.conv(x, w, C, 3, bias=bias, out=out), reps=20, warm=3)
+        fl = 2.0 * B * H * H * N * 9 * C
+        print(json.dumps(dict(kernel="conv3x3", B=B, H=H, C=C, N=N, us=us, tflops=fl / us * 1e-6)), flush=True)
+
+
+if __name__ == "__main__" and "--conv" in sys.argv:
+    conv_bench()
