@@ -126,104 +126,115 @@ __global__ void __launch_bounds__(192, 2)
         for (int k = 0; k < 8; ++k) {
           const uint32_t pa = p_addr + (k >> 2) * TILE + (k & 3) * 32;
           umma_f16(tmem + O_COL, smem_desc(pa, 16, 1024, 2), smem_desc(v_addr + k * 2048, 1024, 1024, 2), idesc_o,
-                   k > 0);
+                   (j | k) > 0);
         }
         umma_commit(o_full);
         umma_commit(v_empty);
       }
     }
   } else {
-    // softmax / correction warps: one thread per query row
+    // softmax / correction warps: one thread per query row. O accumulates in TMEM across KV
+    // blocks (PV_j issued with accumulate=1); the running max used for the exponentials is only
+    // raised when a block's max exceeds it by > 8 (log2 units, i.e. p <= 256), and only then is
+    // O rescaled in TMEM (tcgen05.ld/st) -- with real data that is once or twice per row.
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
-    float m_prev = -INFINITY, l = 0.f, alpha_prev = 1.f;
-    float o_acc[64];
-#pragma unroll
-    for (int i = 0; i < 64; ++i) o_acc[i] = 0.f;
+    float m_used = -INFINITY, l = 0.f;
     uint8_t* prow0 = sP + r * 128;
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(s_full, j & 1);
       tc_fence_after();
       const int kvalid = T - j * 128;  // keys >= kvalid are padding
-      // pass 1: row max over the 128 scores (read from TMEM in 32-column chunks)
-      float mx = m_prev;
+      // pass 1: block row max
+      float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float t[32];
+      for (int c = 0; c < 4; c += 2) {
+        float t[32], u[32];
         tmem_ld32(lane_addr + S_COL + c * 32, t);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i < kvalid) mx = fmaxf(mx, t[i] * scale_log2);
-      }
-      const float alpha = fast_exp2(m_prev - mx);  // m_prev=-inf on the first block -> 0
-      // O_{j-1} must be consumed (and PV_{j-1} finished reading P) before P_j is written
-      if (j > 0) {
-        mbar_wait(o_full, (j - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float t[32];
-          tmem_ld32(lane_addr + O_COL + c * 32, t);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o_acc[c * 32 + i] = o_acc[c * 32 + i] * alpha_prev + t[i];
-        }
-      }
-      alpha_prev = alpha;
-      // pass 2: p = exp2(s*scale - max), row sum, P_j (bf16) into the UMMA SW128 K-major layout
-      float rs = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float t[32];
-        tmem_ld32(lane_addr + S_COL + c * 32, t);
+        tmem_ld32(lane_addr + S_COL + (c + 1) * 32, u);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          t[i] = (c * 32 + i < kvalid) ? fast_exp2(fmaf(t[i], scale_log2, -mx)) : 0.f;
+          if (c * 32 + i < kvalid) mx = fmaxf(mx, t[i] * scale_log2);
+          if ((c + 1) * 32 + i < kvalid) mx = fmaxf(mx, u[i] * scale_log2);
+        }
+      }
+      // PV_{j-1} must be finished (P buffer free, O stable) before P_j / any O rescale
+      if (j > 0) {
+        mbar_wait(o_full, (j - 1) & 1);
+        tc_fence_after();
+      }
+      if (mx > m_used + 8.f) {
+        const float alpha = fast_exp2(m_used - mx);  // 0 on the first block
+        l *= alpha;
+        if (j > 0) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            float t[32];
+            tmem_ld32(lane_addr + O_COL + c * 32, t);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) t[i] *= alpha;
+            tmem_st32(lane_addr + O_COL + c * 32, t);
+          }
+          tmem_st_wait();
+        }
+        m_used = mx;
+      }
+      // pass 2: p = exp2(s*scale - m_used), row sum, P_j (bf16) into the UMMA SW128 K-major layout
+      float rs = 0.f;
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {  // 64 keys (one P tile) per TMEM wait
+        float t[64];
+        tmem_ld32(lane_addr + S_COL + c2 * 64, *reinterpret_cast<float(*)[32]>(t));
+        tmem_ld32(lane_addr + S_COL + c2 * 64 + 32, *reinterpret_cast<float(*)[32]>(t + 32));
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          t[i] = (c2 * 64 + i < kvalid) ? fast_exp2(fmaf(t[i], scale_log2, -m_used)) : 0.f;
           rs += t[i];
         }
-        uint8_t* prow = prow0 + (c >> 1) * TILE;
+        uint8_t* prow = prow0 + c2 * TILE;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int chunk = (c & 1) * 4 + k;  // 16-byte chunk within the 128-byte row
+        for (int k = 0; k < 8; ++k) {  // 16-byte chunk k of the 128-byte row, SW128 position
           uint4 u;
           u.x = pack_bf16(t[8 * k + 0], t[8 * k + 1]);
           u.y = pack_bf16(t[8 * k + 2], t[8 * k + 3]);
           u.z = pack_bf16(t[8 * k + 4], t[8 * k + 5]);
           u.w = pack_bf16(t[8 * k + 6], t[8 * k + 7]);
-          *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) = u;
+          *reinterpret_cast<uint4*>(prow + ((k ^ (r & 7)) << 4)) = u;
         }
       }
-      l = l * alpha + rs;
-      m_prev = mx;
+      l += rs;
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(p_full);
     }
     mbar_wait(o_full, (nkv - 1) & 1);
     tc_fence_after();
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      float t[32];
-      tmem_ld32(lane_addr + O_COL + c * 32, t);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) o_acc[c * 32 + i] = o_acc[c * 32 + i] * alpha_prev + t[i];
-    }
     const int qi = q0 + r;
+    const float inv = 1.f / l;
+    float t[32], u[32];
+    tmem_ld32(lane_addr + O_COL, t);
+    tmem_ld32(lane_addr + O_COL + 32, u);
+    tmem_ld_wait();
     if (qi < T) {
-      const float inv = 1.f / l;
       uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(row_base + qi) * D + head * 64);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint4 u;
-        u.x = pack_bf16(o_acc[8 * c + 0] * inv, o_acc[8 * c + 1] * inv);
-        u.y = pack_bf16(o_acc[8 * c + 2] * inv, o_acc[8 * c + 3] * inv);
-        u.z = pack_bf16(o_acc[8 * c + 4] * inv, o_acc[8 * c + 5] * inv);
-        u.w = pack_bf16(o_acc[8 * c + 6] * inv, o_acc[8 * c + 7] * inv);
-        dst[c] = u;
+      for (int c = 0; c < 4; ++c) {
+        uint4 w;
+        w.x = pack_bf16(t[8 * c + 0] * inv, t[8 * c + 1] * inv);
+        w.y = pack_bf16(t[8 * c + 2] * inv, t[8 * c + 3] * inv);
+        w.z = pack_bf16(t[8 * c + 4] * inv, t[8 * c + 5] * inv);
+        w.w = pack_bf16(t[8 * c + 6] * inv, t[8 * c + 7] * inv);
+        dst[c] = w;
+        uint4 x;
+        x.x = pack_bf16(u[8 * c + 0] * inv, u[8 * c + 1] * inv);
+        x.y = pack_bf16(u[8 * c + 2] * inv, u[8 * c + 3] * inv);
+        x.z = pack_bf16(u[8 * c + 4] * inv, u[8 * c + 5] * inv);
+        x.w = pack_bf16(u[8 * c + 6] * inv, u[8 * c + 7] * inv);
+        dst[4 + c] = x;
       }
     }
   }

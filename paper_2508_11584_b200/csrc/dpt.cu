@@ -198,14 +198,15 @@ static int bind_taps(vpe_dpt* d, const void* const* taps) {
     int N;
     if (i < 2) {
       const int k = i == 0 ? 4 : 2;
-      N = k * k * d->C[i];
+      const int cout_p = (d->C[i] + 31) / 32 * 32;  // weights padded per sub-pixel (heads.py)
+      N = k * k * cout_p;
       e.kind = EPI_CONVT;
       e.N = N;
       e.bias = d->w.rs_b[i];
       e.out = d->r[i];
       e.ldo = d->Cp[i];
       e.ct_k = k;
-      e.ct_cout = d->C[i];
+      e.ct_cout = cout_p;
       e.ct_H = h;
       e.ct_W = h;
     } else {

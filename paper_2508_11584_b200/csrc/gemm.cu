@@ -19,16 +19,20 @@
 
 namespace vpe {
 
-constexpr int EPI_WARPS = 8;
+// EPI_SPLIT warps per TMEM lane quadrant share a tile's 32-column chunks round-robin; more warps
+// per SMSP hide the dependent-FMA / MUFU latency of the GELU epilogue (ncu: "wait" stalls).
+constexpr int EPI_SPLIT = 4;
+constexpr int EPI_WARPS = 4 * EPI_SPLIT;
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
-constexpr int STAGE_BUF = 32 * 32 * 4;  // per epilogue warp: 32 rows x 32 cols x fp32
+// per epilogue warp: 4 KB = two 2-KB halves for bf16 tiles (32x32) or one 4-KB fp32 tile
+constexpr int STAGE_BUF = 32 * 32 * 4;
 
 template <int BN, int BK>
 struct GemmCfg {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int PIPE_BUDGET = 160 * 1024;
+  static constexpr int PIPE_BUDGET = 150 * 1024;
   static constexpr int STAGES_RAW = PIPE_BUDGET / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : ((2 * BN) <= 64 ? 64 : ((2 * BN) <= 128 ? 128 : ((2 * BN) <= 256 ? 256 : 512)));
@@ -196,17 +200,19 @@ VPE_DEV void epilogue_direct(const EpiParams& ep, int64_t gpix, int col0, float 
       const int64_t img = gpix / HW;
       const int rem = (int)(gpix - img * HW);
       const int y = rem / ep.ct_W, x = rem - (rem / ep.ct_W) * ep.ct_W;
+      // ct_cout is a multiple of 32, so a 32-column chunk is 32 contiguous channels of one
+      // output sub-pixel: one 64-byte vector store
       const int k = ep.ct_k, Wo = ep.ct_W * k, Ho = ep.ct_H * k;
-      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(ep.out);
+      const int s = col0 / ep.ct_cout, co0 = col0 - s * ep.ct_cout;
+      const int ky = s / k, kx = s - ky * k;
+      const int64_t op = (img * Ho + (int64_t)(y * k + ky)) * Wo + (x * k + kx);
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(ep.out) + op * ep.ldo + co0;
+      if (full) {
+        store_bf16x32(dst, v);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int c = col0 + j;
-        if (c < N) {
-          const int s = c / ep.ct_cout, co = c - s * ep.ct_cout;
-          const int ky = s / k, kx = s - ky * k;
-          const int64_t op = (img * Ho + (int64_t)(y * k + ky)) * Wo + (x * k + kx);
-          out[op * ep.ldo + co] = __float2bfloat16_rn(v[j]);
-        }
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < N) dst[j] = __float2bfloat16_rn(v[j]);
       }
       break;
     }
@@ -322,12 +328,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else {
-    // epilogue warps 2..9: TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4
+    // epilogue warps: TMEM lane quadrant = warp % 4, column slice = (warp - 2) / 4
     const int e = warp - 2;
     const int q = warp & 3;
     const int chalf = e >> 2;
     const int r = q * 32 + lane;
-    uint8_t* stg = sStage + e * STAGE_BUF;
+    uint8_t* stg_base = sStage + e * STAGE_BUF;
+    int nstore = 0;  // staging double buffer: store n uses half n & 1
     int i = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int acc = i & 1;
@@ -349,12 +356,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
+      if (chalf >= BN / 32) {  // narrow tile: this column slice has no chunk, release at once
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
 #pragma unroll 1
-      for (int c = chalf; c < BN / 32; c += 2) {
+      for (int c = chalf; c < BN / 32; c += EPI_SPLIT) {
         const int c0 = c * 32;
         float v[32];
         tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c0, v);
         tmem_ld_wait();
+        if (c + EPI_SPLIT >= BN / 32) {  // this warp's last TMEM read of the tile: release it now
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
         const int col0 = n0 + c0;
         if (col0 >= p.ep.N) continue;  // warp-uniform
         if (p.tma_out) {
@@ -366,14 +381,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], p.ep.act);
           }
-          if (lane == 0) bulk_wait_read0();  // staging buffer free again
+          const bool bf = p.ep.kind == EPI_BF16;
+          uint8_t* stg = stg_base + (bf ? (nstore & 1) * (STAGE_BUF / 2) : 0);
+          if (lane == 0) {  // the store that last used this buffer has finished reading it
+            if (bf)
+              bulk_wait_read1();
+            else
+              bulk_wait_read0();
+          }
           __syncwarp();
+          // staging rows are written in the TMA swizzle layout (bank-conflict free):
+          // bf16: 64-B rows, SWIZZLE_64B (chunk ^ ((row>>1)&3)); f32: 128-B rows, SWIZZLE_128B
           if (p.ep.kind == EPI_BF16) {
-            store_bf16x32(reinterpret_cast<__nv_bfloat16*>(stg + lane * 64), v);
-          } else {
-            float4* s4 = reinterpret_cast<float4*>(stg + lane * 128);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) s4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            for (int k = 0; k < 4; ++k) {
+              uint4 u;
+              u.x = pack_bf16(v[8 * k + 0], v[8 * k + 1]);
+              u.y = pack_bf16(v[8 * k + 2], v[8 * k + 3]);
+              u.z = pack_bf16(v[8 * k + 4], v[8 * k + 5]);
+              u.w = pack_bf16(v[8 * k + 6], v[8 * k + 7]);
+              *reinterpret_cast<uint4*>(stg + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) = u;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              *reinterpret_cast<float4*>(stg + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+                  make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
           }
           fence_async_smem();
           __syncwarp();
@@ -384,12 +417,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               tma_store_2d(&tout, stg, col0, m0 + q * 32);
             bulk_commit();
           }
+          ++nstore;
         } else if (valid) {
           epilogue_direct(p.ep, gpix, col0, v);
         }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
     }
     if (lane == 0) bulk_wait0();
   }
@@ -548,7 +580,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = chalf; c < BN / 32; c += 2) {
+      for (int c = chalf; c < BN / 32; c += EPI_SPLIT) {
         const int c0 = c * 32;
         float v[32];
         tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c0, v);
@@ -645,7 +677,7 @@ static int make_out_map(GemmPlan* g, int M) {
   uint64_t strides[1] = {(uint64_t)ld * esz};
   uint32_t box[2] = {32u, 32u};
   VPE_TRY(encode_tma_t(&g->tout, bf ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
-                       strides, box, CU_TENSOR_MAP_SWIZZLE_NONE));
+                       strides, box, bf ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B));
   g->p.tma_out = 1;
   return VPE_OK;
 }

@@ -121,15 +121,18 @@ int launch_layernorm(const float* x, int M, int D, const float* w, const float* 
 
 // ---------------------------------------------------------------------------------------------
 // Bilinear resize on NHWC bf16, align_corners=True (modeling_depth_anything.py:157-200, 288-293).
-// Thread = 8 channels of one output pixel. Input/output channel pitch cp (elements), C real.
-__global__ void bilinear_ac_kernel(const __nv_bfloat16* __restrict__ in, int B, int Hi, int Wi, int cp,
-                                   __nv_bfloat16* __restrict__ out, int Ho, int Wo, int C) {
-  const int cv = C / 8;
-  const int64_t total = (int64_t)B * Ho * Wo * cv;
+// Thread = up to 32 channels (4 x 16 B) of one output pixel: the bilinear weights are computed
+// once and 16 independent 16-byte loads are in flight per thread. Channel pitch cp, C real.
+template <int NV>
+__global__ void __launch_bounds__(256) bilinear_ac_kernel(const __nv_bfloat16* __restrict__ in, int B, int Hi,
+                                                          int Wi, int cp, __nv_bfloat16* __restrict__ out, int Ho,
+                                                          int Wo, int C) {
+  const int groups = C / (8 * NV);
+  const int64_t total = (int64_t)B * Ho * Wo * groups;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
-  const int c8 = (int)(t % cv);
-  int64_t pix = t / cv;
+  const int g = (int)(t % groups);
+  int64_t pix = t / groups;
   const int ox = (int)(pix % Wo);
   pix /= Wo;
   const int oy = (int)(pix % Ho);
@@ -141,33 +144,50 @@ __global__ void bilinear_ac_kernel(const __nv_bfloat16* __restrict__ in, int B, 
   const int y1 = y0 + (y0 < Hi - 1), x1 = x0 + (x0 < Wi - 1);
   const float ly = fy - y0, lx = fx - x0;
   const float hy = 1.f - ly, hx = 1.f - lx;
-  const __nv_bfloat16* base = in + (int64_t)b * Hi * Wi * cp + c8 * 8;
-  const uint4 a = *reinterpret_cast<const uint4*>(base + ((int64_t)y0 * Wi + x0) * cp);
-  const uint4 bq = *reinterpret_cast<const uint4*>(base + ((int64_t)y0 * Wi + x1) * cp);
-  const uint4 c = *reinterpret_cast<const uint4*>(base + ((int64_t)y1 * Wi + x0) * cp);
-  const uint4 d = *reinterpret_cast<const uint4*>(base + ((int64_t)y1 * Wi + x1) * cp);
-  const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
-  const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&bq);
-  const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
-  const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d);
-  uint4 o;
-  uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+  const __nv_bfloat16* base = in + (int64_t)b * Hi * Wi * cp + g * 8 * NV;
+  const uint4* p00 = reinterpret_cast<const uint4*>(base + ((int64_t)y0 * Wi + x0) * cp);
+  const uint4* p01 = reinterpret_cast<const uint4*>(base + ((int64_t)y0 * Wi + x1) * cp);
+  const uint4* p10 = reinterpret_cast<const uint4*>(base + ((int64_t)y1 * Wi + x0) * cp);
+  const uint4* p11 = reinterpret_cast<const uint4*>(base + ((int64_t)y1 * Wi + x1) * cp);
+  uint4 a[NV], bq[NV], c[NV], d[NV];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float2 fa = __bfloat1622float2(pa[j]), fb = __bfloat1622float2(pb[j]);
-    const float2 fc = __bfloat1622float2(pc[j]), fd = __bfloat1622float2(pd[j]);
-    const float r0 = hy * (hx * fa.x + lx * fb.x) + ly * (hx * fc.x + lx * fd.x);
-    const float r1 = hy * (hx * fa.y + lx * fb.y) + ly * (hx * fc.y + lx * fd.y);
-    po[j] = pack_bf16(r0, r1);
+  for (int v = 0; v < NV; ++v) {
+    a[v] = __ldg(p00 + v);
+    bq[v] = __ldg(p01 + v);
+    c[v] = __ldg(p10 + v);
+    d[v] = __ldg(p11 + v);
   }
-  *reinterpret_cast<uint4*>(out + (((int64_t)b * Ho + oy) * Wo + ox) * cp + c8 * 8) = o;
+  uint4* dst = reinterpret_cast<uint4*>(out + (((int64_t)b * Ho + oy) * Wo + ox) * cp + g * 8 * NV);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a[v]);
+    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&bq[v]);
+    const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c[v]);
+    const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d[v]);
+    uint4 o;
+    uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 fa = __bfloat1622float2(pa[j]), fb = __bfloat1622float2(pb[j]);
+      const float2 fc = __bfloat1622float2(pc[j]), fd = __bfloat1622float2(pd[j]);
+      const float r0 = hy * (hx * fa.x + lx * fb.x) + ly * (hx * fc.x + lx * fd.x);
+      const float r1 = hy * (hx * fa.y + lx * fb.y) + ly * (hx * fc.y + lx * fd.y);
+      po[j] = pack_bf16(r0, r1);
+    }
+    dst[v] = o;
+  }
 }
 
 int launch_bilinear_ac(const __nv_bfloat16* in, int B, int Hi, int Wi, int cp, __nv_bfloat16* out, int Ho, int Wo,
                        int C, cudaStream_t s) {
   if (C % 8 || cp % 8) return VPE_E_SHAPE;
-  const int64_t total = (int64_t)B * Ho * Wo * (C / 8);
-  bilinear_ac_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(in, B, Hi, Wi, cp, out, Ho, Wo, C);
+  const int nv = (C % 32 == 0) ? 4 : 1;
+  const int64_t total = (int64_t)B * Ho * Wo * (C / (8 * nv));
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  if (nv == 4)
+    bilinear_ac_kernel<4><<<blocks, 256, 0, s>>>(in, B, Hi, Wi, cp, out, Ho, Wo, C);
+  else
+    bilinear_ac_kernel<1><<<blocks, 256, 0, s>>>(in, B, Hi, Wi, cp, out, Ho, Wo, C);
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
 }
 

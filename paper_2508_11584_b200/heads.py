@@ -96,10 +96,15 @@ class DepthHead:
             bp = W[p + "projection.bias"].double()
             if f > 1:
                 k = int(f)
+                cp = (ch + 31) // 32 * 32  # each sub-pixel's channels padded to a 32-column chunk
                 wt = W[p + "resize.weight"].double()  # [C_in, C_out, k, k]
-                m = wt.permute(2, 3, 1, 0).reshape(k * k * ch, ch)  # [(ky,kx,co), c]
+                m = torch.zeros(k, k, cp, ch, dtype=torch.float64)
+                m[:, :, :ch, :] = wt.permute(2, 3, 1, 0)  # [(ky,kx,co), c]
+                m = m.reshape(k * k * cp, ch)
+                bt = torch.zeros(cp, dtype=torch.float64)
+                bt[:ch] = W[p + "resize.bias"].double()
                 wc.rs_w[i] = pk.bf16(m @ wp)
-                wc.rs_b[i] = pk.f32(m @ bp + W[p + "resize.bias"].double().repeat(k * k))
+                wc.rs_b[i] = pk.f32(m @ bp + bt.repeat(k * k))
             else:
                 wc.rs_w[i] = pk.bf16(wp)
                 wc.rs_b[i] = pk.f32(bp)
