@@ -175,6 +175,10 @@ def run_reference(args):
                                    f"(baseline/_ref) + fp32 oracle compute, {threads} torch threads"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+    # the reference's shared-memory arena raises BufferError from __del__ at interpreter exit
+    # while numpy views are alive (fanpipe/arena.py:269-276); the result is printed, leave quietly
+    sys.stderr.flush()
+    os._exit(0)
 
 
 # ------------------------------------------------------------------------------------------------

@@ -37,24 +37,15 @@ __device__ __forceinline__ void src_index(float scale, int dst, int in_size, int
   l0 = 1.f - l1;
 }
 
-constexpr int CC = 32;                                            // classes per pass
-constexpr int NPT = (14 * BAND_COLS + SEG_THREADS - 1) / SEG_THREADS;  // output pixels per thread
-
-// Separable form of torch's bilinear (align_corners=False) followed by argmax:
-//   out = (x00*w0 + x01*w1)*h0 + (x10*w0 + x11*w1)*h1  ==  A(y0)*h0 + A(y1)*h1,
-//   A(y) = x(y,x0)*w0 + x(y,x1)*w1  (the x-interpolated source row, same rounding order).
-// A is computed once per CTA for the 3 source rows a band touches and shared by its 14
-// output rows; classes are swept in chunks with the running (max, argmax) kept in registers.
 __global__ void __launch_bounds__(SEG_THREADS)
     seg_upsample_argmax_kernel(const float* __restrict__ logits, int h, int C, int cp, int R,
                                uint8_t* __restrict__ labels) {
-  extern __shared__ float s_mem[];
-  float* s_log = s_mem;                      // [3 rows][10 cols][C] source window
-  float* s_row = s_mem + 3 * 10 * C;         // [3 rows][CC][BAND_COLS] x-interpolated rows
+  extern __shared__ float s_log[];  // [3 rows][10 cols][C]
   const int band = blockIdx.x, chunk = blockIdx.y, b = blockIdx.z;
   const int rows_per_band = R / h;  // 14
   const float scale = (float)h / (float)R;
   const int oy0 = band * rows_per_band, ox0 = chunk * BAND_COLS;
+  // source window (rows band-1..band+1, cols 8*chunk-1 .. 8*chunk+8), clamped
   const int sy0 = max(band - 1, 0);
   const int sx0 = max(chunk * (BAND_COLS / rows_per_band) - 1, 0);
   const int wcols = 10, wrows = 3;
@@ -64,57 +55,32 @@ __global__ void __launch_bounds__(SEG_THREADS)
     const int yy = sy0 + pix / wcols, xx = sx0 + pix % wcols;
     s_log[i] = (yy < h && xx < h) ? src[((int64_t)yy * h + xx) * cp + c] : 0.f;
   }
-  float best[NPT];
-  int arg[NPT];
-#pragma unroll
-  for (int k = 0; k < NPT; ++k) {
-    best[k] = -INFINITY;
-    arg[k] = 0;
-  }
+  __syncthreads();
   const int npx = rows_per_band * BAND_COLS;
-  for (int c0 = 0; c0 < C; c0 += CC) {
-    const int ncc = min(CC, C - c0);
-    __syncthreads();  // s_log ready / previous chunk's s_row consumed
-    for (int i = threadIdx.x; i < wrows * CC * BAND_COLS; i += blockDim.x) {
-      const int ox = i % BAND_COLS, rc = i / BAND_COLS;
-      const int cc = rc % CC, yy = rc / CC;
-      if (cc >= ncc) continue;
-      int x0, x1;
-      float wx0, wx1;
-      src_index(scale, min(ox0 + ox, R - 1), h, x0, x1, wx0, wx1);
-      const float* row = s_log + yy * wcols * C + c0 + cc;
-      s_row[i] = __fadd_rn(__fmul_rn(row[(x0 - sx0) * C], wx0), __fmul_rn(row[(x1 - sx0) * C], wx1));
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < NPT; ++k) {
-      const int p = threadIdx.x + k * SEG_THREADS;
-      if (p >= npx) continue;
-      const int oy = oy0 + p / BAND_COLS, ox = p % BAND_COLS;
-      int y0, y1;
-      float hy0, hy1;
-      src_index(scale, min(oy, R - 1), h, y0, y1, hy0, hy1);
-      const float* a0 = s_row + (y0 - sy0) * CC * BAND_COLS + ox;
-      const float* a1 = s_row + (y1 - sy0) * CC * BAND_COLS + ox;
-      float bv = best[k];
-      int ba = arg[k];
-      for (int cc = 0; cc < ncc; ++cc) {
-        const float v = __fadd_rn(__fmul_rn(a0[cc * BAND_COLS], hy0), __fmul_rn(a1[cc * BAND_COLS], hy1));
-        if (v > bv) {
-          bv = v;
-          ba = c0 + cc;
-        }
-      }
-      best[k] = bv;
-      arg[k] = ba;
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < NPT; ++k) {
-    const int p = threadIdx.x + k * SEG_THREADS;
-    if (p >= npx) continue;
+  for (int p = threadIdx.x; p < npx; p += blockDim.x) {
     const int oy = oy0 + p / BAND_COLS, ox = ox0 + p % BAND_COLS;
-    if (oy < R && ox < R) labels[((int64_t)b * R + oy) * R + ox] = (uint8_t)arg[k];
+    if (oy >= R || ox >= R) continue;
+    int y0, y1, x0, x1;
+    float hy0, hy1, wx0, wx1;
+    src_index(scale, oy, h, y0, y1, hy0, hy1);
+    src_index(scale, ox, h, x0, x1, wx0, wx1);
+    const float* r00 = s_log + ((y0 - sy0) * wcols + (x0 - sx0)) * C;
+    const float* r01 = s_log + ((y0 - sy0) * wcols + (x1 - sx0)) * C;
+    const float* r10 = s_log + ((y1 - sy0) * wcols + (x0 - sx0)) * C;
+    const float* r11 = s_log + ((y1 - sy0) * wcols + (x1 - sx0)) * C;
+    float best = -INFINITY;
+    int arg = 0;
+    for (int c = 0; c < C; ++c) {
+      // torch CPU order: (x00*w0 + x01*w1)*h0 + (x10*w0 + x11*w1)*h1
+      const float t0 = __fadd_rn(__fmul_rn(r00[c], wx0), __fmul_rn(r01[c], wx1));
+      const float t1 = __fadd_rn(__fmul_rn(r10[c], wx0), __fmul_rn(r11[c], wx1));
+      const float v = __fadd_rn(__fmul_rn(t0, hy0), __fmul_rn(t1, hy1));
+      if (v > best) {
+        best = v;
+        arg = c;
+      }
+    }
+    labels[((int64_t)b * R + oy) * R + ox] = (uint8_t)arg;
   }
 }
 }  // namespace
@@ -162,13 +128,7 @@ extern "C" int vpe_seg_forward(vpe_seg* s, const void* final_tap, uint8_t* label
   VPE_TRY(launch_gemm(s->g, st));
   const int R = s->cfg.resolution;
   dim3 grid(h, (R + BAND_COLS - 1) / BAND_COLS, B);
-  const size_t smem = ((size_t)3 * 10 * C + 3 * CC * BAND_COLS) * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)((3 * 10 * 256 + 3 * CC * BAND_COLS) * sizeof(float))));
-    attr = true;
-  }
+  const size_t smem = (size_t)3 * 10 * C * sizeof(float);
   seg_upsample_argmax_kernel<<<grid, SEG_THREADS, smem, st>>>(s->logits, h, C, s->cpitch, R, labels);
   VPE_CUDA_TRY(cudaGetLastError());
   count_launches(2);
