@@ -444,24 +444,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 // "virtual" positions v = ry*P + rx of the padded row pitch P; the 2 halo columns per row are
 // computed and discarded by the epilogue.
 // ------------------------------------------------------------------------------------------
-template <int BN, int KC>
+// RT = output rows of 128 pixels per tile (W >= 128 only): RT accumulators of 128 x BN share one
+// (RT+2)-row halo, so the A traffic per output row drops from 3 to (RT+2)/RT halo rows.
+template <int BN, int KC, int RT>
 struct HaloCfg {
   static constexpr int GCH = 8 * KC;                 // channels per group
-  static constexpr int A_MAX = KC * 130 * 3 * 16;    // largest halo stage (P=130, 3 rows)
+  static constexpr int A_MAX = KC * 130 * (RT + 2) * 16;  // largest halo stage (P=130)
   static constexpr int A_STAGES = 2;
   static constexpr int B_BYTES = BN * GCH * 2;       // one tap's weight tile
   static constexpr int B_STAGES = BN >= 128 ? 4 : 8;
-  static constexpr int TMEM_COLS = GemmCfg<BN, 64>::TMEM_COLS;
+  static constexpr int TMEM_COLS = GemmCfg<BN * RT, 64>::TMEM_COLS;
   static constexpr int B_SWZ = GCH == 64 ? 2 : 4;
   static constexpr int B_SBO = 8 * GCH * 2;
   static constexpr size_t SMEM = 1024 + (size_t)A_STAGES * A_MAX + (size_t)B_STAGES * B_BYTES + 256;
 };
 
-template <int BN, int KC>
+template <int BN, int KC, int RT>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                      const GemmParams p) {
-  using C = HaloCfg<BN, KC>;
+  using C = HaloCfg<BN, KC, RT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem;  // 1024-aligned for the swizzled weight tiles
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int acc = i & 1;
         mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
+        const uint32_t d = tmem + acc * BN * RT;
         bool first = true;
         for (int g = 0; g < groups; ++g, ++ia) {
           const int sa = ia % C::A_STAGES;
@@ -547,15 +549,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tc_fence_after();
             const int tap = j % 9;
             const int dy = tap / 3, dx = tap - (tap / 3) * 3;
-            const uint32_t at = a0 + (uint32_t)((dy * P + dx) * 16);
             const uint32_t b0 = smem_u32(sB + sb * C::B_BYTES);
 #pragma unroll
-            for (int k = 0; k < KC / 2; ++k) {
-              const uint64_t ad = smem_desc(at + 2 * k * chunk_stride, chunk_stride, 128, 0);
-              const uint64_t bd = smem_desc(b0 + k * 32, 16, C::B_SBO, C::B_SWZ);
-              umma_f16(d, ad, bd, idesc, first ? 0u : 1u);
-              first = false;
+            for (int rt = 0; rt < RT; ++rt) {
+              const uint32_t at = a0 + (uint32_t)(((rt + dy) * P + dx) * 16);
+#pragma unroll
+              for (int k = 0; k < KC / 2; ++k) {
+                const uint64_t ad = smem_desc(at + 2 * k * chunk_stride, chunk_stride, 128, 0);
+                const uint64_t bd = smem_desc(b0 + k * 32, 16, C::B_SBO, C::B_SWZ);
+                umma_f16(d + rt * BN, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+              }
             }
+            first = false;
             umma_commit(&b_empty[sb]);
           }
           umma_commit(&a_empty[sa]);
@@ -567,24 +572,26 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int e = warp - 2;
     const int q = warp & 3;
     const int chalf = e >> 2;
-    const int r = q * 32 + lane;  // virtual output position within the tile
+    const int r = q * 32 + lane;  // virtual output position within a 128-row sub-tile
     const int ry = r / P, rx = r - (r / P) * P;
+    const int rows_sub = p.bh / RT;  // output rows per 128-row sub-tile (1 when RT > 1)
     int i = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
       const int acc = i & 1;
       const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
       const int img = mt / p.tiles_per_img, rr = mt - img * p.tiles_per_img;
-      const int y = (rr / p.tiles_x) * p.bh + ry, x = (rr % p.tiles_x) * p.bw + rx;
-      const bool valid = ry < p.bh && rx < p.bw && y < p.H && x < p.W;
-      const int64_t gpix = ((int64_t)img * p.H + y) * p.W + x;
+      const int ytile = (rr / p.tiles_x) * p.bh, x = (rr % p.tiles_x) * p.bw + rx;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = chalf; c < BN / 32; c += EPI_SPLIT) {
-        const int c0 = c * 32;
+      for (int k = chalf; k < RT * (BN / 32); k += EPI_SPLIT) {
+        const int rt = k / (BN / 32), c0 = (k - rt * (BN / 32)) * 32;
         float v[32];
-        tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c0, v);
+        tmem_ld32(tmem + (acc * RT + rt) * BN + ((uint32_t)(q * 32) << 16) + c0, v);
         tmem_ld_wait();
+        const int y = ytile + rt * rows_sub + ry;
+        const bool valid = ry < rows_sub && rx < p.bw && y < p.H && x < p.W;
+        const int64_t gpix = ((int64_t)img * p.H + y) * p.W + x;
         const int col0 = nt * BN + c0;
         if (valid && col0 < p.ep.N) epilogue_direct(p.ep, gpix, col0, v);
       }
@@ -774,18 +781,22 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   } else if (Cp % 64) {
     return VPE_E_SHAPE;
   }
-  int bw, P, rows;
+  int bw, P, rows, rt = 1;
   if (W >= 128) {
     bw = 128;
     P = 130;
-    rows = 1;
+    // stack RT output rows on one halo when the channel group is narrow (A traffic per output
+    // row (RT+2)/RT); keep the 2 x RT x BN TMEM columns and the two halo stages within budget
+    if (kc == 4 && bn == 32) rt = 4;
+    else if (kc == 8 && bn <= 64) rt = 2;
+    rows = rt;
   } else {
     bw = W;
     P = W + 2;
     rows = 128 / P;
   }
-  if (rows < 1 || (double)(rows * bw) / 128.0 < 0.7) return VPE_E_SHAPE;
-  const int rows_box = 129 / P + 3;
+  if (rows < 1 || (double)(rows * bw) / (128.0 * rt) < 0.7) return VPE_E_SHAPE;
+  const int rows_box = rt > 1 ? rt + 2 : 129 / P + 3;
   if (P > 256 || rows_box > 256) return VPE_E_SHAPE;
   if ((pitch_px * 2) % 16 || (pitch_row * 2) % 16 || (pitch_img * 2) % 16 || reinterpret_cast<uintptr_t>(X) % 16)
     return VPE_E_SHAPE;
@@ -816,22 +827,24 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   g->bn = bn;
   g->bk = gch;
   g->halo_kc = kc;
-#define VPE_HS(BN_, KC_) \
-  if (bn == BN_ && kc == KC_) g->smem = HaloCfg<BN_, KC_>::SMEM;
-  VPE_HS(32, 4) VPE_HS(64, 4) VPE_HS(128, 4) VPE_HS(32, 8) VPE_HS(64, 8) VPE_HS(128, 8)
+  g->halo_rt = rt;
+#define VPE_HS(BN_, KC_, RT_) \
+  if (bn == BN_ && kc == KC_ && rt == RT_) g->smem = HaloCfg<BN_, KC_, RT_>::SMEM;
+  VPE_HS(32, 4, 1) VPE_HS(64, 4, 1) VPE_HS(128, 4, 1) VPE_HS(32, 8, 1) VPE_HS(64, 8, 1) VPE_HS(128, 8, 1)
+  VPE_HS(32, 4, 4) VPE_HS(32, 8, 2) VPE_HS(64, 8, 2)
 #undef VPE_HS
   return VPE_OK;
 }
 
-template <int BN, int KC>
+template <int BN, int KC, int RT>
 static int launch_halo_t(const GemmPlan& g, cudaStream_t s) {
-  auto k = conv_halo_kernel<BN, KC>;
+  auto k = conv_halo_kernel<BN, KC, RT>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg<BN, KC>::SMEM);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg<BN, KC, RT>::SMEM);
     attr_set = true;
   }
-  k<<<g.grid, GEMM_THREADS, HaloCfg<BN, KC>::SMEM, s>>>(g.ta, g.tb, g.p);
+  k<<<g.grid, GEMM_THREADS, HaloCfg<BN, KC, RT>::SMEM, s>>>(g.ta, g.tb, g.p);
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
 }
 
@@ -849,9 +862,10 @@ static int launch_t(const GemmPlan& g, cudaStream_t s) {
 
 int launch_gemm(const GemmPlan& g, cudaStream_t s) {
   if (g.halo_kc) {
-#define VPE_LH(BN_, KC_) \
-  if (g.bn == BN_ && g.halo_kc == KC_) return launch_halo_t<BN_, KC_>(g, s);
-    VPE_LH(32, 4) VPE_LH(64, 4) VPE_LH(128, 4) VPE_LH(32, 8) VPE_LH(64, 8) VPE_LH(128, 8)
+#define VPE_LH(BN_, KC_, RT_) \
+  if (g.bn == BN_ && g.halo_kc == KC_ && g.halo_rt == RT_) return launch_halo_t<BN_, KC_, RT_>(g, s);
+    VPE_LH(32, 4, 1) VPE_LH(64, 4, 1) VPE_LH(128, 4, 1) VPE_LH(32, 8, 1) VPE_LH(64, 8, 1) VPE_LH(128, 8, 1)
+    VPE_LH(32, 4, 4) VPE_LH(32, 8, 2) VPE_LH(64, 8, 2)
 #undef VPE_LH
     return VPE_E_SHAPE;
   }

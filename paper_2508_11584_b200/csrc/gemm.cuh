@@ -68,7 +68,8 @@ struct GemmPlan {
   GemmParams p;
   dim3 grid;
   int bn = 0, bk = 0;
-  int halo_kc = 0;  // > 0: conv_halo_kernel<bn, halo_kc>
+  int halo_kc = 0;  // > 0: conv_halo_kernel<bn, halo_kc, halo_rt>
+  int halo_rt = 1;
   size_t smem = 0;
 };
 

@@ -69,12 +69,14 @@ def test_linear_split_precision(ops, device):
     assert rel_l2(out.cpu().double(), ref) < 1e-5
 
 
-@pytest.mark.parametrize("B,T,heads", [(1, 257, 6), (1, 1025, 6), (2, 1370, 12), (1, 128, 2), (3, 200, 4)])
-def test_attention(ops, device, B, T, heads):
+@pytest.mark.parametrize("B,T,heads", [(1, 257, 6), (1, 1025, 6), (2, 1370, 12), (1, 128, 2), (3, 200, 4),
+                                       (2, 300, 2)])
+@pytest.mark.parametrize("variant", ["pingpong", "single"])
+def test_attention(ops, device, B, T, heads, variant):
     D = heads * 64
     g = torch.Generator().manual_seed(T)
-    qkv = torch.randn(B * T, 3 * D, generator=g).to(device, torch.bfloat16)
-    out = ops.attention(qkv, B, T, D, heads)
+    qkv = (torch.randn(B * T, 3 * D, generator=g) * 2).to(device, torch.bfloat16)
+    out = ops.attention(qkv, B, T, D, heads if variant == "pingpong" else -heads)
     q, k, v = qkv.float().view(B, T, 3, heads, 64).permute(2, 0, 3, 1, 4)
     ref = torch.softmax(q @ k.transpose(-1, -2) / 8.0, -1) @ v
     ref = ref.transpose(1, 2).reshape(B * T, D)
