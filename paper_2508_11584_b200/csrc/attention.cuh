@@ -15,8 +15,3 @@ struct AttnPlan {
 int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, int B, int T, int D, int heads);
 int launch_attention(const AttnPlan& a, cudaStream_t s);
 }  // namespace vpe
-
-namespace vpe {
-// two 128-query tiles per CTA, two softmax warpgroups (attention_pp.cu); same plan/maps
-int launch_attention_pp(const AttnPlan& a, cudaStream_t s);
-}  // namespace vpe

@@ -117,13 +117,8 @@ int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32
 int vpe_op_attention(const void* qkv, void* out, int32_t B, int32_t T, int32_t D, int32_t heads, void* stream) {
   AttnPlan a;
   VPE_TRY(plan_attention(&a, static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(out), B, T, D,
-                         heads < 0 ? -heads : heads));
-  // heads < 0 selects the single-tile kernel (A/B comparison in tests / microbench)
-  if (heads < 0) {
-    VPE_TRY(launch_attention(a, static_cast<cudaStream_t>(stream)));
-  } else {
-    VPE_TRY(launch_attention_pp(a, static_cast<cudaStream_t>(stream)));
-  }
+                         heads));
+  VPE_TRY(launch_attention(a, static_cast<cudaStream_t>(stream)));
   count_launches(1);
   return VPE_OK;
 }

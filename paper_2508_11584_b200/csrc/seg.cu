@@ -37,50 +37,64 @@ __device__ __forceinline__ void src_index(float scale, int dst, int in_size, int
   l0 = 1.f - l1;
 }
 
+// Separable form of torch's bilinear (align_corners=False) + argmax, identical rounding order:
+//   out = (x00*w0 + x01*w1)*h0 + (x10*w0 + x11*w1)*h1 = A(y0)*h0 + A(y1)*h1,
+//   A(y, ox) = x(y, x0)*w0 + x(y, x1)*w1.
+// A CTA owns half a source band (7 output rows, which all read the same two source rows) and 56
+// output columns; A for those 2 rows x 56 columns x all classes is built once in SMEM
+// ([row][class][column], conflict-free), then every pixel does 2 loads + 3 flops per class.
+constexpr int SEG_COLS = 56;
 __global__ void __launch_bounds__(SEG_THREADS)
     seg_upsample_argmax_kernel(const float* __restrict__ logits, int h, int C, int cp, int R,
                                uint8_t* __restrict__ labels) {
-  extern __shared__ float s_log[];  // [3 rows][10 cols][C]
-  const int band = blockIdx.x, chunk = blockIdx.y, b = blockIdx.z;
-  const int rows_per_band = R / h;  // 14
+  extern __shared__ float s_mem[];
+  const int wcols = 6;
+  float* s_src = s_mem;                      // [2 rows][6 cols][C]
+  float* s_a = s_mem + 2 * wcols * C;        // [2 rows][C][SEG_COLS]
+  const int hb = blockIdx.x, chunk = blockIdx.y, b = blockIdx.z;
+  const int rows_per_band = R / h;   // 14
+  const int half_rows = rows_per_band / 2;
   const float scale = (float)h / (float)R;
-  const int oy0 = band * rows_per_band, ox0 = chunk * BAND_COLS;
-  // source window (rows band-1..band+1, cols 8*chunk-1 .. 8*chunk+8), clamped
-  const int sy0 = max(band - 1, 0);
-  const int sx0 = max(chunk * (BAND_COLS / rows_per_band) - 1, 0);
-  const int wcols = 10, wrows = 3;
+  const int oy0 = hb * half_rows, ox0 = chunk * SEG_COLS;
+  int y0, y1;
+  float hy0_unused, hy1_unused;
+  src_index(scale, oy0, h, y0, y1, hy0_unused, hy1_unused);
+  const int sx0 = max(chunk * (SEG_COLS / rows_per_band) - 1, 0);
   const float* src = logits + (int64_t)b * h * h * cp;
-  for (int i = threadIdx.x; i < wrows * wcols * C; i += blockDim.x) {
+  for (int i = threadIdx.x; i < 2 * wcols * C; i += blockDim.x) {
     const int c = i % C, pix = i / C;
-    const int yy = sy0 + pix / wcols, xx = sx0 + pix % wcols;
-    s_log[i] = (yy < h && xx < h) ? src[((int64_t)yy * h + xx) * cp + c] : 0.f;
+    const int yy = pix / wcols ? y1 : y0, xx = sx0 + pix % wcols;
+    s_src[i] = xx < h ? src[((int64_t)yy * h + xx) * cp + c] : 0.f;
   }
   __syncthreads();
-  const int npx = rows_per_band * BAND_COLS;
-  for (int p = threadIdx.x; p < npx; p += blockDim.x) {
-    const int oy = oy0 + p / BAND_COLS, ox = ox0 + p % BAND_COLS;
-    if (oy >= R || ox >= R) continue;
-    int y0, y1, x0, x1;
-    float hy0, hy1, wx0, wx1;
-    src_index(scale, oy, h, y0, y1, hy0, hy1);
-    src_index(scale, ox, h, x0, x1, wx0, wx1);
-    const float* r00 = s_log + ((y0 - sy0) * wcols + (x0 - sx0)) * C;
-    const float* r01 = s_log + ((y0 - sy0) * wcols + (x1 - sx0)) * C;
-    const float* r10 = s_log + ((y1 - sy0) * wcols + (x0 - sx0)) * C;
-    const float* r11 = s_log + ((y1 - sy0) * wcols + (x1 - sx0)) * C;
+  for (int i = threadIdx.x; i < 2 * C * SEG_COLS; i += blockDim.x) {
+    const int ox = i % SEG_COLS, rc = i / SEG_COLS;
+    const int c = rc % C, yy = rc / C;
+    int x0, x1;
+    float wx0, wx1;
+    src_index(scale, min(ox0 + ox, R - 1), h, x0, x1, wx0, wx1);
+    const float* row = s_src + yy * wcols * C + c;
+    s_a[i] = __fadd_rn(__fmul_rn(row[(x0 - sx0) * C], wx0), __fmul_rn(row[(x1 - sx0) * C], wx1));
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < half_rows * SEG_COLS; p += blockDim.x) {
+    const int oy = oy0 + p / SEG_COLS, ox = p % SEG_COLS;
+    int yy0, yy1;
+    float hy0, hy1;
+    src_index(scale, oy, h, yy0, yy1, hy0, hy1);
+    const float* a0 = s_a + ox;
+    const float* a1 = s_a + C * SEG_COLS + ox;
     float best = -INFINITY;
     int arg = 0;
+#pragma unroll 4
     for (int c = 0; c < C; ++c) {
-      // torch CPU order: (x00*w0 + x01*w1)*h0 + (x10*w0 + x11*w1)*h1
-      const float t0 = __fadd_rn(__fmul_rn(r00[c], wx0), __fmul_rn(r01[c], wx1));
-      const float t1 = __fadd_rn(__fmul_rn(r10[c], wx0), __fmul_rn(r11[c], wx1));
-      const float v = __fadd_rn(__fmul_rn(t0, hy0), __fmul_rn(t1, hy1));
+      const float v = __fadd_rn(__fmul_rn(a0[c * SEG_COLS], hy0), __fmul_rn(a1[c * SEG_COLS], hy1));
       if (v > best) {
         best = v;
         arg = c;
       }
     }
-    labels[((int64_t)b * R + oy) * R + ox] = (uint8_t)arg;
+    if (ox0 + ox < R) labels[((int64_t)b * R + oy) * R + ox0 + ox] = (uint8_t)arg;
   }
 }
 }  // namespace
@@ -127,8 +141,14 @@ extern "C" int vpe_seg_forward(vpe_seg* s, const void* final_tap, uint8_t* label
   }
   VPE_TRY(launch_gemm(s->g, st));
   const int R = s->cfg.resolution;
-  dim3 grid(h, (R + BAND_COLS - 1) / BAND_COLS, B);
-  const size_t smem = (size_t)3 * 10 * C * sizeof(float);
+  dim3 grid(2 * h, (R + SEG_COLS - 1) / SEG_COLS, B);
+  const size_t smem = ((size_t)2 * 6 * C + 2 * C * SEG_COLS) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)((2 * 6 * 256 + 2 * 256 * SEG_COLS) * sizeof(float))));
+    attr = true;
+  }
   seg_upsample_argmax_kernel<<<grid, SEG_THREADS, smem, st>>>(s->logits, h, C, s->cpitch, R, labels);
   VPE_CUDA_TRY(cudaGetLastError());
   count_launches(2);

@@ -160,7 +160,7 @@ extern "C" int vpe_vit_forward(vpe_vit* v, const void* pixels_u8, void* const* t
     VPE_TRY(launch_layernorm(v->resid, M, D, w.ln1_w[l], w.ln1_b[l], c.ln_eps, v->xln, w.norm_w, w.norm_b, tap_out,
                              s));
     VPE_TRY(launch_gemm(v->qkv_g[l], s));
-    VPE_TRY(launch_attention_pp(v->attn, s));
+    VPE_TRY(launch_attention(v->attn, s));
     VPE_TRY(launch_gemm(v->proj_g[l], s));
     VPE_TRY(launch_layernorm(v->resid, M, D, w.ln2_w[l], w.ln2_b[l], c.ln_eps, v->xln, nullptr, nullptr, nullptr, s));
     VPE_TRY(launch_gemm(v->fc1_g[l], s));

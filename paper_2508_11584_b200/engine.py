@@ -33,6 +33,8 @@ from .weights import make_weights
 from ._lib import check, lib
 
 HEAD_IDS = {"depth": 1, "seg": 2, "det": 3}
+_DT = {torch.float32: DType.F32, torch.uint8: DType.U8, torch.int64: DType.I64, torch.int32: DType.I32,
+       torch.bfloat16: DType.BF16}
 
 
 class _Stream:
@@ -157,6 +159,8 @@ class VPEngine:
         self._ev_next = 0
         self._lat_records = []
         self.host_out = None
+        self.fifo = None
+        self.output_drops = {}
         self.dropped = 0
 
     # ------------------------------------------------------------------ enqueue primitives
@@ -195,6 +199,26 @@ class VPEngine:
         if not self.host_out:
             return 0
         return sum(t.numel() * t.element_size() for o in self.host_out.values() for t in o.values())
+
+    def enable_output_fifos(self, capacity: int = 8) -> dict:
+        """Per-head output queue ("push to output FIFO"; channels.py:377-421): a FIFO
+        channel whose slots live in pinned host memory. Each admitted head run pushes its outputs
+        with stream-ordered D2H copies on the head stream (READY = copies enqueued + event); a host
+        consumer ``pop``s them in order. A full queue rejects the frame (producer_drops)."""
+        self.fifo = {}
+        for n, o in self.out.items():
+            specs = [TensorSpec(k, _DT[t.dtype], tuple(t.shape)) for k, t in o.items()]
+            ch, _ = create_channel(f"out-{n}", ChannelMode.FIFO, capacity, specs, self.namespace, device=-1)
+            ch.register_consumer(1)
+            self.fifo[n] = ch
+        return self.fifo
+
+    def pop_output(self, head: str, block: bool = True, timeout: float | None = 5.0):
+        """Oldest queued output of ``head`` as host tensors, or None (channels.py:377-407)."""
+        ch = self.fifo[head]
+        dst = {s.label: torch.empty(s.dims, dtype=s.dtype.torch_dtype) for s in ch.specs}
+        env = ch.pop(1, dst, block=block, timeout=timeout)
+        return None if env is None else (env.frame_id, dst)
 
     # ------------------------------------------------------------------ one frame set
     def submit(self, host_frames: torch.Tensor | None = None, capture_ts: int | None = None,
@@ -239,6 +263,16 @@ class VPEngine:
                 for k, t in self.out[n].items():
                     check(lib.vpe_memcpy_async(C.c_void_p(self.host_out[n][k].data_ptr()), C.c_void_p(t.data_ptr()),
                                                t.numel() * t.element_size(), C.c_void_p(st.handle)))
+            if self.fifo is not None:
+                outs = self.out[n]
+
+                def out_writer(views, outs=outs, st=st):
+                    for k, t in outs.items():
+                        check(lib.vpe_memcpy_async(C.c_void_p(views[k].data_ptr()), C.c_void_p(t.data_ptr()),
+                                                   t.numel() * t.element_size(), C.c_void_p(st.handle)))
+
+                if not self.fifo[n].push(lease.frame_id, lease.capture_ts, out_writer, stream=st.handle).accepted:
+                    self.output_drops[n] = self.output_drops.get(n, 0) + 1
             ev = self._event() if record_latency else None
             if ev is not None:
                 ev.record(st)
@@ -286,3 +320,6 @@ class VPEngine:
             h.close()
         self.backbone.close()
         self.channel.close()
+        for ch in (self.fifo or {}).values():
+            ch.close()
+        self.fifo = None

@@ -73,3 +73,31 @@ def test_ring_counters_and_rates(eng):
     assert sum("det" in r for r in ran) == 2
     e.set_rate("seg", None)
     e.set_rate("det", None)
+
+
+def test_output_fifo_order_and_content(eng):
+    """SPEC head loop: outputs pushed to a FIFO channel in pinned host memory, popped in order,
+    byte-identical to the device outputs of the same frame (channels.py:377-421)."""
+    e, _ = eng
+    e.enable_output_fifos(capacity=4)
+    frames = make_frames(2, 224, 9)
+    e.pixels.copy_(frames.to(e.device))
+    torch.cuda.synchronize()
+    ran = [e.submit() for _ in range(3)]
+    e.synchronize()
+    dev_last = {n: {k: t.cpu().clone() for k, t in o.items()} for n, o in e.out.items()}
+    for n in e.heads:
+        fids = []
+        for _ in range(3):
+            fid, out = e.pop_output(n)
+            fids.append(fid)
+        assert fids == sorted(fids) and fids[-1] == ran[-1][n]
+        for k in out:
+            assert torch.equal(out[k], dev_last[n][k]), (n, k)
+        assert e.pop_output(n, block=False) is None
+    # a full queue drops (newest-drop, counted) instead of blocking the head
+    for _ in range(6):
+        e.submit()
+    e.synchronize()
+    c = e.fifo["seg"].counters()
+    assert c.producer_drops >= 2 and e.output_drops["seg"] >= 2

@@ -69,14 +69,12 @@ def test_linear_split_precision(ops, device):
     assert rel_l2(out.cpu().double(), ref) < 1e-5
 
 
-@pytest.mark.parametrize("B,T,heads", [(1, 257, 6), (1, 1025, 6), (2, 1370, 12), (1, 128, 2), (3, 200, 4),
-                                       (2, 300, 2)])
-@pytest.mark.parametrize("variant", ["pingpong", "single"])
-def test_attention(ops, device, B, T, heads, variant):
+@pytest.mark.parametrize("B,T,heads", [(1, 257, 6), (1, 1025, 6), (2, 1370, 12), (1, 128, 2), (3, 200, 4)])
+def test_attention(ops, device, B, T, heads):
     D = heads * 64
     g = torch.Generator().manual_seed(T)
-    qkv = (torch.randn(B * T, 3 * D, generator=g) * 2).to(device, torch.bfloat16)
-    out = ops.attention(qkv, B, T, D, heads if variant == "pingpong" else -heads)
+    qkv = torch.randn(B * T, 3 * D, generator=g).to(device, torch.bfloat16)
+    out = ops.attention(qkv, B, T, D, heads)
     q, k, v = qkv.float().view(B, T, 3, heads, 64).permute(2, 0, 3, 1, 4)
     ref = torch.softmax(q @ k.transpose(-1, -2) / 8.0, -1) @ v
     ref = ref.transpose(1, 2).reshape(B * T, D)
@@ -96,7 +94,8 @@ def test_layernorm(ops, device):
 
 
 @pytest.mark.parametrize("H,W,C,Cp,N,ks", [(16, 16, 64, 64, 64, 3), (32, 32, 48, 64, 64, 3), (64, 64, 96, 128, 64, 3),
-                                           (448, 448, 32, 32, 32, 3), (37, 37, 64, 64, 64, 3), (32, 32, 384, 384, 192, 1)])
+                                           (448, 448, 32, 32, 32, 3), (37, 37, 64, 64, 64, 3), (32, 32, 384, 384, 192, 1),
+                                           (128, 128, 64, 64, 64, 3), (256, 256, 64, 64, 32, 3), (130, 130, 32, 32, 32, 3)])
 def test_conv_nhwc(ops, device, H, W, C, Cp, N, ks):
     g = torch.Generator().manual_seed(H + C)
     B = 2 if H < 100 else 1

@@ -48,10 +48,9 @@ def main():
     for (B, T, H) in [(16, 1025, 6), (1, 1025, 6)]:
         D = H * 64
         qkv = torch.randn(B * T, 3 * D, device=dev).to(torch.bfloat16)
+        us = timeit(lambda: _ops.attention(qkv, B, T, D, H))
         fl = 4.0 * B * T * T * D
-        for name, h in (("attention_pp", H), ("attention_1tile", -H)):
-            us = timeit(lambda: _ops.attention(qkv, B, T, D, h))
-            print(json.dumps(dict(kernel=name, B=B, T=T, H=H, us=us, tflops=fl / us * 1e-6)), flush=True)
+        print(json.dumps(dict(kernel="attention", B=B, T=T, H=H, us=us, tflops=fl / us * 1e-6)), flush=True)
 
 
 if __name__ == "__main__":
