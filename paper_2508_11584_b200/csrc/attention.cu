@@ -1,6 +1,8 @@
-// Non-causal multi-head attention (head_dim 64) on tcgen05: S = Q K^T and O_j = P_j V_j run on
-// the tensor cores with both accumulators in TMEM; softmax runs on 4 warps, one thread per
-// query row, with the online max/sum rescale applied in registers.
+// Non-causal multi-head attention (head_dim 64) on tcgen05: S = Q K^T and O += P V run on the
+// tensor cores with both accumulators in TMEM; softmax runs on 4 warps, one thread per query row;
+// O is rescaled in TMEM only when the running max jumps (see the softmax branch below).
+// Tried and measured slower on B200 (round 1): a two-Q-tile ping-pong CTA (265 vs 112 us at B=16)
+// and S-in-registers with early S release + polynomial exp2 (148 us, register-capped with spills).
 //
 // Oracle: transformers modeling_dinov2.py:153-178 (eager softmax(QK^T * 1/8) V).
 // Q/K/V are read in place from the fused QKV GEMM output [B*T, 3D] through a 2D TMA map

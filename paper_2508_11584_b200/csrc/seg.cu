@@ -23,8 +23,6 @@ struct vpe_seg {
 };
 
 namespace {
-constexpr int BAND_COLS = 112;  // output columns per CTA (8 source cells)
-constexpr int SEG_THREADS = 256;
 
 // source index per torch's area_pixel_compute_source_index (align_corners=False, no cubic)
 __device__ __forceinline__ void src_index(float scale, int dst, int in_size, int& i0, int& i1, float& l0,
@@ -37,65 +35,61 @@ __device__ __forceinline__ void src_index(float scale, int dst, int in_size, int
   l0 = 1.f - l1;
 }
 
-// Separable form of torch's bilinear (align_corners=False) + argmax, identical rounding order:
-//   out = (x00*w0 + x01*w1)*h0 + (x10*w0 + x11*w1)*h1 = A(y0)*h0 + A(y1)*h1,
-//   A(y, ox) = x(y, x0)*w0 + x(y, x1)*w1.
-// A CTA owns half a source band (7 output rows, which all read the same two source rows) and 56
-// output columns; A for those 2 rows x 56 columns x all classes is built once in SMEM
-// ([row][class][column], conflict-free), then every pixel does 2 loads + 3 flops per class.
-constexpr int SEG_COLS = 56;
-__global__ void __launch_bounds__(SEG_THREADS)
+// Fused bilinear (align_corners=False) upsample + argmax, torch's rounding order
+//   out = (x00*w0 + x01*w1)*h0 + (x10*w0 + x11*w1)*h1.
+// A CTA owns half a source band: the 7 output rows that all read the same two source rows, every
+// output column of them (one thread per column). Per class a thread loads the 4 corner logits
+// once, forms the two x-interpolations once and reuses them for its 7 output pixels, keeping 7
+// running (max, argmax) pairs in registers; the [C, R, R] logit volume never exists.
+constexpr int HALF_ROWS = 7;  // R / h / 2
+__global__ void __launch_bounds__(1024)
     seg_upsample_argmax_kernel(const float* __restrict__ logits, int h, int C, int cp, int R,
                                uint8_t* __restrict__ labels) {
-  extern __shared__ float s_mem[];
-  const int wcols = 6;
-  float* s_src = s_mem;                      // [2 rows][6 cols][C]
-  float* s_a = s_mem + 2 * wcols * C;        // [2 rows][C][SEG_COLS]
-  const int hb = blockIdx.x, chunk = blockIdx.y, b = blockIdx.z;
-  const int rows_per_band = R / h;   // 14
-  const int half_rows = rows_per_band / 2;
+  extern __shared__ float s_src[];  // [2 rows][h cols][C]
+  const int hb = blockIdx.x, b = blockIdx.y;
   const float scale = (float)h / (float)R;
-  const int oy0 = hb * half_rows, ox0 = chunk * SEG_COLS;
+  const int oy0 = hb * HALF_ROWS;
   int y0, y1;
   float hy0_unused, hy1_unused;
   src_index(scale, oy0, h, y0, y1, hy0_unused, hy1_unused);
-  const int sx0 = max(chunk * (SEG_COLS / rows_per_band) - 1, 0);
   const float* src = logits + (int64_t)b * h * h * cp;
-  for (int i = threadIdx.x; i < 2 * wcols * C; i += blockDim.x) {
+  for (int i = threadIdx.x; i < 2 * h * C; i += blockDim.x) {
     const int c = i % C, pix = i / C;
-    const int yy = pix / wcols ? y1 : y0, xx = sx0 + pix % wcols;
-    s_src[i] = xx < h ? src[((int64_t)yy * h + xx) * cp + c] : 0.f;
+    const int yy = pix / h ? y1 : y0, xx = pix % h;
+    s_src[i] = src[((int64_t)yy * h + xx) * cp + c];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 2 * C * SEG_COLS; i += blockDim.x) {
-    const int ox = i % SEG_COLS, rc = i / SEG_COLS;
-    const int c = rc % C, yy = rc / C;
-    int x0, x1;
-    float wx0, wx1;
-    src_index(scale, min(ox0 + ox, R - 1), h, x0, x1, wx0, wx1);
-    const float* row = s_src + yy * wcols * C + c;
-    s_a[i] = __fadd_rn(__fmul_rn(row[(x0 - sx0) * C], wx0), __fmul_rn(row[(x1 - sx0) * C], wx1));
+  const int ox = threadIdx.x;
+  if (ox >= R) return;
+  int x0, x1;
+  float wx0, wx1;
+  src_index(scale, ox, h, x0, x1, wx0, wx1);
+  float hy0[HALF_ROWS], hy1[HALF_ROWS], best[HALF_ROWS];
+  int arg[HALF_ROWS];
+#pragma unroll
+  for (int k = 0; k < HALF_ROWS; ++k) {
+    int a0, a1;
+    src_index(scale, oy0 + k, h, a0, a1, hy0[k], hy1[k]);
+    best[k] = -INFINITY;
+    arg[k] = 0;
   }
-  __syncthreads();
-  for (int p = threadIdx.x; p < half_rows * SEG_COLS; p += blockDim.x) {
-    const int oy = oy0 + p / SEG_COLS, ox = p % SEG_COLS;
-    int yy0, yy1;
-    float hy0, hy1;
-    src_index(scale, oy, h, yy0, yy1, hy0, hy1);
-    const float* a0 = s_a + ox;
-    const float* a1 = s_a + C * SEG_COLS + ox;
-    float best = -INFINITY;
-    int arg = 0;
-#pragma unroll 4
-    for (int c = 0; c < C; ++c) {
-      const float v = __fadd_rn(__fmul_rn(a0[c * SEG_COLS], hy0), __fmul_rn(a1[c * SEG_COLS], hy1));
-      if (v > best) {
-        best = v;
-        arg = c;
+  const float* r0 = s_src;
+  const float* r1 = s_src + h * C;
+#pragma unroll 2
+  for (int c = 0; c < C; ++c) {
+    const float t0 = __fadd_rn(__fmul_rn(r0[x0 * C + c], wx0), __fmul_rn(r0[x1 * C + c], wx1));
+    const float t1 = __fadd_rn(__fmul_rn(r1[x0 * C + c], wx0), __fmul_rn(r1[x1 * C + c], wx1));
+#pragma unroll
+    for (int k = 0; k < HALF_ROWS; ++k) {
+      const float v = __fadd_rn(__fmul_rn(t0, hy0[k]), __fmul_rn(t1, hy1[k]));
+      if (v > best[k]) {
+        best[k] = v;
+        arg[k] = c;
       }
     }
-    if (ox0 + ox < R) labels[((int64_t)b * R + oy) * R + ox0 + ox] = (uint8_t)arg;
   }
+#pragma unroll
+  for (int k = 0; k < HALF_ROWS; ++k) labels[((int64_t)b * R + oy0 + k) * R + ox] = (uint8_t)arg[k];
 }
 }  // namespace
 
@@ -141,15 +135,16 @@ extern "C" int vpe_seg_forward(vpe_seg* s, const void* final_tap, uint8_t* label
   }
   VPE_TRY(launch_gemm(s->g, st));
   const int R = s->cfg.resolution;
-  dim3 grid(2 * h, (R + SEG_COLS - 1) / SEG_COLS, B);
-  const size_t smem = ((size_t)2 * 6 * C + 2 * C * SEG_COLS) * sizeof(float);
+  dim3 grid(2 * h, B);
+  const size_t smem = (size_t)2 * h * C * sizeof(float);
   static bool attr = false;
   if (!attr) {
     VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)((2 * 6 * 256 + 2 * 256 * SEG_COLS) * sizeof(float))));
+                                      227 * 1024));
     attr = true;
   }
-  seg_upsample_argmax_kernel<<<grid, SEG_THREADS, smem, st>>>(s->logits, h, C, s->cpitch, R, labels);
+  if (R > 1024 || R != 14 * h || smem > 227 * 1024) return VPE_E_CONFIG;
+  seg_upsample_argmax_kernel<<<grid, (R + 31) / 32 * 32, smem, st>>>(s->logits, h, C, s->cpitch, R, labels);
   VPE_CUDA_TRY(cudaGetLastError());
   count_launches(2);
   if (logits_out) {
