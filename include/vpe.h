@@ -270,6 +270,9 @@ int vpe_stream_wait_event(void* stream, void* ev);
 int vpe_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
 int64_t vpe_kernel_launches(void);    /* kernels enqueued by libvpe since load (graph replays count per node) */
 const char* vpe_status_str(int status);
+/* diagnostics: timeline of attention CTA 0 when the process runs with VPE_ATT_TRACE=1
+   ((code, clock64) pairs; see csrc/attention.cu) */
+int vpe_debug_att_trace(unsigned long long* host, int32_t n);
 
 #ifdef __cplusplus
 }

@@ -1,13 +1,28 @@
-// Non-causal multi-head attention (head_dim 64) on tcgen05: S = Q K^T and O += P V run on the
-// tensor cores with both accumulators in TMEM; softmax runs on 4 warps, one thread per query row;
-// O is rescaled in TMEM only when the running max jumps (see the softmax branch below).
-// Tried and measured slower on B200 (round 1): a two-Q-tile ping-pong CTA (265 vs 112 us at B=16)
-// and S-in-registers with early S release + polynomial exp2 (148 us, register-capped with spills).
+// Non-causal multi-head attention (head_dim 64) on tcgen05, one persistent CTA per SM.
 //
 // Oracle: transformers modeling_dinov2.py:153-178 (eager softmax(QK^T * 1/8) V).
-// Q/K/V are read in place from the fused QKV GEMM output [B*T, 3D] through a 2D TMA map
+// Q/K/V are read in place from the fused QKV GEMM output [B*T, 3D] through one 2D TMA map
 // (box 64 cols x 128 rows), so no head re-layout pass is needed.
+//
+// Work unit = (image, head, pair of 128-row Q tiles). The two Q tiles share every K/V tile the
+// producer brings in, and run ping-pong on the tensor core:
+//   warp 0      TMA producer: Q_A, Q_B per unit (double-buffered across units), then K_j / V_j
+//               through 3-stage rings
+//   warps 1, 2  MMA issuers, one per Q slot X: S_X(j+1) = Q_X K_{j+1}^T as soon as softmax X has
+//               pulled S_X(j) into registers; O_X += P_X(j) V_j with P read from TMEM (.kind::f16
+//               A-from-TMEM), so P never touches shared memory
+//   warp 3      idle (completes warpgroup 0)
+//   warps 4-7   softmax A, warps 8-11 softmax B: one thread per query row, the whole 128-key S
+//               row in registers; tree max / tree sum; p = 2^(s*scale - m) written to TMEM as
+//               bf16 pairs; O is rescaled in TMEM only when the running max rises by > 8 (log2),
+//               i.e. almost never after the first KV tile.
+// TMEM (512 columns): S_A | S_B | P_A | P_B | O_A | O_B.
+// Rows/keys past T (tail tiles) are computed on whatever the TMA brought (the next image's rows
+// or zero fill) and masked: invalid keys get p = 0, invalid rows are never stored, and warps whose
+// 32 rows are all past T skip the exponentials.
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "attention.cuh"
 #include "tc.cuh"
@@ -17,234 +32,500 @@ namespace vpe {
 
 namespace {
 constexpr int TILE = 16 * 1024;  // one [128][64] bf16 SW128 tile
-// Q + K double-buffered + V single-buffered + P: 96 KB -> two CTAs per SM, so one CTA's
-// softmax overlaps the other's tensor-core work (ncu: 1 CTA/SM left the tensor pipe 88% idle)
-constexpr int SMEM_ATT = 1024 + TILE /*Q*/ + 2 * TILE /*K*/ + TILE /*V*/ + 2 * TILE /*P*/ + 256;
-constexpr int S_COL = 0, O_COL = 128, TMEM_COLS = 256;
+constexpr int KS = 3, VS = 3;    // K / V ring depth
+constexpr int ATT_THREADS = 384;  // 0 TMA, 1-2 MMA (slot A / B), 3 idle, 4-7 softmax A, 8-11 softmax B
+constexpr int SMEM_ATT = 1024 + 4 * TILE /*Q_A,Q_B x 2 units*/ + KS * TILE + VS * TILE + 256;
+constexpr uint32_t S_COL = 0, P_COL = 256, O_COL = 384;
 }  // namespace
 
-__global__ void __launch_bounds__(192, 2)
-    attention_tc_kernel(const __grid_constant__ CUtensorMap tqkv, __nv_bfloat16* __restrict__ out, int T, int D,
-                        float scale_log2) {
+VPE_DEV void tmem_st32u(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+VPE_DEV void tmem_st16u(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// O[tmem] (+)= A[tmem] * B[smem], kind::f16; A (M x K, K-major, 2 bf16 per 32-bit column)
+VPE_DEV void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// ---- softmax arithmetic: f32x2 SIMD (FFMA2/FADD2), 3-input max, exp2 split between MUFU and an
+// FMA-pipe polynomial, bf16 packing by byte permute (no F2FP on the XU pipe).
+VPE_DEV uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+VPE_DEV void f2_unpack(uint64_t r, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+VPE_DEV uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+VPE_DEV uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+VPE_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// tcgen05.wait::ld that also ties the loaded registers, so no use of them can be scheduled
+// above the wait
+VPE_DEV void tmem_ld_wait_dep(float (&v)[32]) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
+VPE_DEV float chunk_max_log2(const float (&v)[32], float scale_log2) {
+  float m0 = fmax3(v[0], v[1], v[2]), m1 = fmax3(v[3], v[4], v[5]);
+#pragma unroll
+  for (int i = 6; i < 30; i += 4) {
+    m0 = fmax3(m0, v[i], v[i + 1]);
+    m1 = fmax3(m1, v[i + 2], v[i + 3]);
+  }
+  return fmax3(m0, m1, fmaxf(v[30], v[31])) * scale_log2;
+}
+
+// 2^x for a pair, x <= 8, on the FMA pipe: x = n + f (n = rint(x), |f| <= 1/2), 2^f by a cubic
+// (max rel. error 1.4e-4, far below the bf16 rounding of P), 2^n by adding n to the exponent.
+VPE_DEV uint64_t exp2_poly2(uint64_t x) {
+  float x0, x1;
+  f2_unpack(x, x0, x1);
+  x = f2_pack(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+  const float kMagic = 12582912.f;  // 1.5 * 2^23: x + kMagic holds rint(x) in its low mantissa bits
+  const uint64_t j = fadd2(x, f2_pack(kMagic, kMagic));
+  const uint64_t nf = fadd2(j, f2_pack(-kMagic, -kMagic));
+  const uint64_t f = ffma2(nf, f2_pack(-1.f, -1.f), x);
+  uint64_t p = ffma2(f, f2_pack(0.05502927f, 0.05502927f), f2_pack(0.24225698f, 0.24225698f));
+  p = ffma2(p, f, f2_pack(0.69325305f, 0.69325305f));
+  p = ffma2(p, f, f2_pack(0.99995134f, 0.99995134f));
+  const uint32_t jl = (uint32_t)j, jh = (uint32_t)(j >> 32);
+  const uint32_t pl = (uint32_t)p, ph = (uint32_t)(p >> 32);
+  return ((uint64_t)(ph + (jh << 23)) << 32) | (uint64_t)(pl + (jl << 23));
+}
+
+// P in bf16 by truncation (one PRMT per pair). The exponent offset carries +log2(1 + 0.00282),
+// the mean relative truncation loss of bf16, so the kept P is unbiased; l is corrected by the
+// same factor in the epilogue.
+constexpr float kTruncBias = 0.0040625f;     // log2(1.00282)
+constexpr float kTruncScale = 1.00282f;
+
+// p = 2^(v*scale - m) for one 32-key chunk -> 16 bf16 pairs in TMEM at p_taddr; returns the
+// chunk's f32x2 partial sums. poly_ok: chunk has no masked (-inf) keys.
+template <int kPolyMask>  // pairs (of 16 per chunk) whose exp2 runs on the FMA pipe
+VPE_DEV uint64_t emit_chunk(const float (&v)[32], float scale_log2, float m_used, uint32_t p_taddr, bool poly_ok) {
+  const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
+  const float mb = kTruncBias - m_used;
+  const uint64_t mb2 = f2_pack(mb, mb);
+  uint64_t acc0 = 0, acc1 = 0;
+  uint32_t pk[16];
+  if (poly_ok) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint64_t xx = ffma2(f2_pack(v[2 * i], v[2 * i + 1]), sc2, mb2);
+      uint64_t pp;
+      if ((kPolyMask >> i) & 1) {
+        pp = exp2_poly2(xx);
+      } else {
+        float x0, x1;
+        f2_unpack(xx, x0, x1);
+        pp = f2_pack(fast_exp2(x0), fast_exp2(x1));
+      }
+      if (i & 1) acc1 = fadd2(acc1, pp); else acc0 = fadd2(acc0, pp);
+      pk[i] = __byte_perm((uint32_t)pp, (uint32_t)(pp >> 32), 0x7632);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint64_t xx = ffma2(f2_pack(v[2 * i], v[2 * i + 1]), sc2, mb2);
+      float x0, x1;
+      f2_unpack(xx, x0, x1);
+      const uint64_t pp = f2_pack(fast_exp2(x0), fast_exp2(x1));
+      if (i & 1) acc1 = fadd2(acc1, pp); else acc0 = fadd2(acc0, pp);
+      pk[i] = __byte_perm((uint32_t)pp, (uint32_t)(pp >> 32), 0x7632);
+    }
+  }
+  tmem_st16u(p_taddr, pk);
+  return fadd2(acc0, acc1);
+}
+
+// ---- optional timeline trace of CTA 0 (diagnostics only: VPE_ATT_TRACE=1, read back with
+// vpe_debug_att_trace). Slots: [0,2048) MMA thread, [2048,3072) softmax A, [3072,4096) softmax B;
+// each event = (code, clock64).
+__device__ unsigned long long g_att_trace[4096];
+static int g_att_trace_on = -1;
+#define ATT_TRACE(slot_base, idx, code)                                              \
+  do {                                                                               \
+    if (trace && blockIdx.x == 0 && (idx) < 510) {                                   \
+      g_att_trace[(slot_base) + 2 * (idx)] = (unsigned long long)(code);             \
+      g_att_trace[(slot_base) + 2 * (idx) + 1] = (unsigned long long)clock64();      \
+      ++(idx);                                                                       \
+    }                                                                                \
+  } while (0)
+
+struct AttnUnit {
+  int b, h, q0, has_b;
+};
+
+VPE_DEV AttnUnit unit_of(int u, int BH, int heads, int T) {
+  // pair-major ordering: every (image, head) pair-0 first, ..., so the (cheap) tail pairs run last
+  AttnUnit r;
+  const int pair = u / BH, bh = u - pair * BH;
+  r.b = bh / heads;
+  r.h = bh - r.b * heads;
+  r.q0 = pair * 256;
+  r.has_b = (r.q0 + 128) < T;
+  return r;
+}
+
+template <int POLY>
+__global__ void __launch_bounds__(ATT_THREADS, 1)
+    attention_tc_kernel(const __grid_constant__ CUtensorMap tqkv, __nv_bfloat16* __restrict__ out, int B, int T,
+                        int D, int heads, float scale_log2, int trace) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + TILE;
-  uint8_t* sV = sK + 2 * TILE;
-  uint8_t* sP = sV + TILE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * TILE);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* k_empty = bars + 3;  // [2] freed when S_j completes
-  uint64_t* v_full = bars + 5;
-  uint64_t* v_empty = bars + 6;  // freed when PV_j completes
-  uint64_t* s_full = bars + 7;
-  uint64_t* p_full = bars + 8;
-  uint64_t* o_full = bars + 9;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint8_t* sQ = smem;               // [2 units][2 slots]: the next unit's Q lands during this one
+  uint8_t* sK = sQ + 4 * TILE;      // [KS]
+  uint8_t* sV = sK + KS * TILE;     // [VS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VS * TILE);
+  uint64_t* q_full = bars;          // [2 units][2 slots]
+  uint64_t* q_empty = bars + 4;     // [2 units][2 slots]
+  uint64_t* k_full = bars + 8;      // [KS]
+  uint64_t* k_empty = k_full + KS;  // [KS]  released by both MMA issuers
+  uint64_t* v_full = k_empty + KS;  // [VS]
+  uint64_t* v_empty = v_full + VS;  // [VS]  released by both MMA issuers
+  uint64_t* s_full = v_empty + VS;  // [2]
+  uint64_t* s_free = s_full + 2;    // [2] softmax x has pulled S_x into registers
+  uint64_t* p_full = s_free + 2;    // [2]
+  uint64_t* o_done = p_full + 2;    // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 2);
 
-  const int qt = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
-  const int q0 = qt * 128;
-  const int row_base = b * T;
+  const int BH = B * heads;
+  const int npairs = (T + 255) / 256;
+  const int units = BH * npairs;
   const int nkv = (T + 127) / 128;
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tqkv);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
     }
-    mbar_init(v_full, 1);
-    mbar_init(v_empty, 1);
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
-    mbar_init(o_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_done[i], 1);
+    }
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 2);
+    }
+    for (int i = 0; i < VS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 2);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tslot, TMEM_COLS);
+  if (warp == 1) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
+  // Units are ordered pair-major, so a unit without a B tile (T <= q0 + 128) is followed only by
+  // such units: the slot-B barriers are simply left alone from then on.
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, TILE);
-      tma_load_2d(sQ, &tqkv, q_full, head * 64, row_base + q0);
-      mbar_expect_tx(&k_full[0], TILE);
-      tma_load_2d(sK, &tqkv, &k_full[0], D + head * 64, row_base);
-      // order K_{j+1} before V_j: K_{j+1} only waits for S_{j-1}, V_j waits for PV_{j-1}
-      for (int j = 0; j < nkv; ++j) {
-        if (j + 1 < nkv) {
-          const int s = (j + 1) & 1;
-          mbar_wait(&k_empty[s], (((j + 1) >> 1) & 1) ^ 1);
-          mbar_expect_tx(&k_full[s], TILE);
-          tma_load_2d(sK + s * TILE, &tqkv, &k_full[s], D + head * 64, row_base + (j + 1) * 128);
+      int kit = 0, vit = 0, qn = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++qn) {
+        const AttnUnit w = unit_of(u, BH, heads, T);
+        const int row0 = w.b * T;
+        const int qb = qn & 1;
+        for (int x = 0; x < 1 + w.has_b; ++x) {
+          mbar_wait(&q_empty[qb * 2 + x], ((qn >> 1) & 1) ^ 1);
+          mbar_expect_tx(&q_full[qb * 2 + x], TILE);
+          tma_load_2d(sQ + (qb * 2 + x) * TILE, &tqkv, &q_full[qb * 2 + x], w.h * 64, row0 + w.q0 + x * 128);
         }
-        mbar_wait(v_empty, (j & 1) ^ 1);
-        mbar_expect_tx(v_full, TILE);
-        tma_load_2d(sV, &tqkv, v_full, 2 * D + head * 64, row_base + j * 128);
+        for (int j = 0; j < nkv; ++j, ++kit, ++vit) {
+          const int ks = kit % KS, vs = vit % VS;
+          mbar_wait(&k_empty[ks], ((kit / KS) & 1) ^ 1);
+          mbar_expect_tx(&k_full[ks], TILE);
+          tma_load_2d(sK + ks * TILE, &tqkv, &k_full[ks], D + w.h * 64, row0 + j * 128);
+          mbar_wait(&v_empty[vs], ((vit / VS) & 1) ^ 1);
+          mbar_expect_tx(&v_full[vs], TILE);
+          tma_load_2d(sV + vs * TILE, &tqkv, &v_full[vs], 2 * D + w.h * 64, row0 + j * 128);
+        }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 2) {
+    // one MMA issuer per Q slot, so neither slot's PV/S issue queues behind the other's
     if (lane == 0) {
+      const int x = warp - 1;
       constexpr uint32_t idesc_s = idesc_bf16(128, 128);
       constexpr uint32_t idesc_o = idesc_bf16(128, 64, /*b_mn_major=*/true);
-      const uint32_t q_addr = smem_u32(sQ);
-      mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
-      tc_fence_after();
-      {
-        const uint32_t k_addr = smem_u32(sK);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          umma_f16(tmem + S_COL, smem_desc(q_addr + k * 32, 16, 1024, 2), smem_desc(k_addr + k * 32, 16, 1024, 2),
-                   idesc_s, k > 0);
-        umma_commit(s_full);
-        umma_commit(&k_empty[0]);
-      }
-      for (int j = 0; j < nkv; ++j) {
-        mbar_wait(p_full, j & 1);
-        tc_fence_after();
-        if (j + 1 < nkv) {
-          const int s1 = (j + 1) & 1;
-          mbar_wait(&k_full[s1], ((j + 1) >> 1) & 1);
+      int kit = 0, vit = 0, qn = 0, np = 0;  // np: PV MMAs issued (= p_full / s_free phases consumed)
+      const uint32_t s_t = tmem + S_COL + x * 128, p_t = tmem + P_COL + x * 64, o_t = tmem + O_COL + x * 64;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++qn) {
+        const AttnUnit w = unit_of(u, BH, heads, T);
+        const bool mine = (x == 0) || w.has_b;
+        const int qi = (qn & 1) * 2 + x;
+        if (mine) {
+          mbar_wait(&q_full[qi], (qn >> 1) & 1);
           tc_fence_after();
-          const uint32_t k_addr = smem_u32(sK + s1 * TILE);
+        }
+        const uint32_t q_addr = smem_u32(sQ + qi * TILE);
+        // S_x = Q_x K^T. The previous S_x was released (s_free / p_full waited) before the
+        // previous PV, so the S_x columns are free here.
+        auto issue_s = [&](uint32_t k_addr) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            umma_f16(tmem + S_COL, smem_desc(q_addr + k * 32, 16, 1024, 2), smem_desc(k_addr + k * 32, 16, 1024, 2),
-                     idesc_s, k > 0);
-          umma_commit(s_full);
-          umma_commit(&k_empty[s1]);
-        }
-        mbar_wait(v_full, j & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(sV);
-        const uint32_t p_addr = smem_u32(sP);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t pa = p_addr + (k >> 2) * TILE + (k & 3) * 32;
-          umma_f16(tmem + O_COL, smem_desc(pa, 16, 1024, 2), smem_desc(v_addr + k * 2048, 1024, 1024, 2), idesc_o,
-                   (j | k) > 0);
-        }
-        umma_commit(o_full);
-        umma_commit(v_empty);
-      }
-    }
-  } else {
-    // softmax / correction warps: one thread per query row. O accumulates in TMEM across KV
-    // blocks (PV_j issued with accumulate=1); the running max used for the exponentials is only
-    // raised when a block's max exceeds it by > 8 (log2 units, i.e. p <= 256), and only then is
-    // O rescaled in TMEM (tcgen05.ld/st) -- with real data that is once or twice per row.
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
-    float m_used = -INFINITY, l = 0.f;
-    uint8_t* prow0 = sP + r * 128;
-    for (int j = 0; j < nkv; ++j) {
-      mbar_wait(s_full, j & 1);
-      tc_fence_after();
-      const int kvalid = T - j * 128;  // keys >= kvalid are padding
-      // pass 1: block row max
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 4; c += 2) {
-        float t[32], u[32];
-        tmem_ld32(lane_addr + S_COL + c * 32, t);
-        tmem_ld32(lane_addr + S_COL + (c + 1) * 32, u);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (c * 32 + i < kvalid) mx = fmaxf(mx, t[i] * scale_log2);
-          if ((c + 1) * 32 + i < kvalid) mx = fmaxf(mx, u[i] * scale_log2);
-        }
-      }
-      // PV_{j-1} must be finished (P buffer free, O stable) before P_j / any O rescale
-      if (j > 0) {
-        mbar_wait(o_full, (j - 1) & 1);
-        tc_fence_after();
-      }
-      if (mx > m_used + 8.f) {
-        const float alpha = fast_exp2(m_used - mx);  // 0 on the first block
-        l *= alpha;
-        if (j > 0) {
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            float t[32];
-            tmem_ld32(lane_addr + O_COL + c * 32, t);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) t[i] *= alpha;
-            tmem_st32(lane_addr + O_COL + c * 32, t);
+            umma_f16(s_t, smem_desc(q_addr + k * 32, 16, 1024, 2), smem_desc(k_addr + k * 32, 16, 1024, 2), idesc_s,
+                     k > 0);
+          umma_commit(&s_full[x]);
+        };
+        for (int j = 0; j < nkv; ++j, ++vit) {
+          if (j == 0) {  // S_x(0)
+            const int ks = kit % KS;
+            mbar_wait(&k_full[ks], (kit / KS) & 1);
+            tc_fence_after();
+            if (mine) issue_s(smem_u32(sK + ks * TILE));
+            if (nkv > 1) {  // K_0 stays until S_x(0) is done; with nkv == 1 it is released below
+              if (mine) umma_commit(&k_empty[ks]); else mbar_arrive(&k_empty[ks]);
+              ++kit;
+            }
           }
-          tmem_st_wait();
+          const bool next = j + 1 < nkv;
+          const int ks = kit % KS, vs = vit % VS;
+          if (next) mbar_wait(&k_full[ks], (kit / KS) & 1);
+          mbar_wait(&v_full[vs], (vit / VS) & 1);
+          tc_fence_after();
+          if (mine) {
+            if (next) {
+              mbar_wait(&s_free[x], np & 1);  // S_x(j) is in softmax registers: S_x(j+1) may land
+              tc_fence_after();
+              issue_s(smem_u32(sK + ks * TILE));
+            }
+            mbar_wait(&p_full[x], np & 1);  // P_x(j) in TMEM
+            tc_fence_after();
+            ++np;
+            const uint32_t v_addr = smem_u32(sV + vs * TILE);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              umma_f16_ts(o_t, p_t + k * 8, smem_desc(v_addr + k * 2048, 1024, 1024, 2), idesc_o,
+                          (j > 0 || k > 0) ? 1u : 0u);
+            umma_commit(&o_done[x]);
+            if (next || nkv == 1) umma_commit(&k_empty[ks]);
+            umma_commit(&v_empty[vs]);
+            if (!next) umma_commit(&q_empty[qi]);  // every S_x of the unit issued
+          } else {
+            if (next || nkv == 1) mbar_arrive(&k_empty[ks]);
+            mbar_arrive(&v_empty[vs]);
+          }
+          if (next || nkv == 1) ++kit;
         }
-        m_used = mx;
       }
-      // pass 2: p = exp2(s*scale - m_used), row sum, P_j (bf16) into the UMMA SW128 K-major layout
-      float rs = 0.f;
-#pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2) {  // 64 keys (one P tile) per TMEM wait
-        float t[64];
-        tmem_ld32(lane_addr + S_COL + c2 * 64, *reinterpret_cast<float(*)[32]>(t));
-        tmem_ld32(lane_addr + S_COL + c2 * 64 + 32, *reinterpret_cast<float(*)[32]>(t + 32));
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          t[i] = (c2 * 64 + i < kvalid) ? fast_exp2(fmaf(t[i], scale_log2, -m_used)) : 0.f;
-          rs += t[i];
-        }
-        uint8_t* prow = prow0 + c2 * TILE;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {  // 16-byte chunk k of the 128-byte row, SW128 position
-          uint4 u;
-          u.x = pack_bf16(t[8 * k + 0], t[8 * k + 1]);
-          u.y = pack_bf16(t[8 * k + 2], t[8 * k + 3]);
-          u.z = pack_bf16(t[8 * k + 4], t[8 * k + 5]);
-          u.w = pack_bf16(t[8 * k + 6], t[8 * k + 7]);
-          *reinterpret_cast<uint4*>(prow + ((k ^ (r & 7)) << 4)) = u;
-        }
-      }
-      l += rs;
-      fence_async_smem();
-      tc_fence_before();
-      mbar_arrive(p_full);
     }
-    mbar_wait(o_full, (nkv - 1) & 1);
-    tc_fence_after();
-    const int qi = q0 + r;
-    const float inv = 1.f / l;
-    float t[32], u[32];
-    tmem_ld32(lane_addr + O_COL, t);
-    tmem_ld32(lane_addr + O_COL + 32, u);
-    tmem_ld_wait();
-    if (qi < T) {
-      uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(row_base + qi) * D + head * 64);
+  } else if (warp == 3) {
+    // idle: completes warpgroup 0
+  } else {
+    // softmax warps: x = Q slot, quadrant = warp % 4 (TMEM lanes 32*quadrant ..)
+    const int x = (warp >= 8) ? 1 : 0;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    const uint32_t s_addr = lane_base + S_COL + x * 128;
+    const uint32_t p_addr = lane_base + P_COL + x * 64;
+    const uint32_t o_addr = lane_base + O_COL + x * 64;
+    int ns = 0, npv = 0;  // S tiles consumed, P tiles produced (global counts)
+    int tn = 0;
+    const bool tr = (quad == 0 && lane == 0);
+    const int tbase = 2048 + 1024 * x;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const AttnUnit w = unit_of(u, BH, heads, T);
+      if (x == 1 && !w.has_b) continue;
+      const int q0 = w.q0 + x * 128;
+      const bool warp_active = (q0 + quad * 32) < T;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkv; ++j, ++ns, ++npv) {
+        if (tr) ATT_TRACE(tbase, tn, 10);
+        mbar_wait(&s_full[x], ns & 1);
+        tc_fence_after();
+        if (tr) ATT_TRACE(tbase, tn, 11);
+        auto release_s = [&]() {  // every load of S_x(j) has landed in registers
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_free[x]);
+        };
+        if (warp_active) {
+          const int kvalid = T - j * 128;  // keys >= kvalid are padding / the next image
+          const int nch = kvalid >= 128 ? 4 : (kvalid + 31) >> 5;  // chunks holding a valid key
+          auto mask = [&](int c, float (&v)[32]) {
+            if (c * 32 + 32 > kvalid) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint4 w;
-        w.x = pack_bf16(t[8 * c + 0] * inv, t[8 * c + 1] * inv);
-        w.y = pack_bf16(t[8 * c + 2] * inv, t[8 * c + 3] * inv);
-        w.z = pack_bf16(t[8 * c + 4] * inv, t[8 * c + 5] * inv);
-        w.w = pack_bf16(t[8 * c + 6] * inv, t[8 * c + 7] * inv);
-        dst[c] = w;
-        uint4 x;
-        x.x = pack_bf16(u[8 * c + 0] * inv, u[8 * c + 1] * inv);
-        x.y = pack_bf16(u[8 * c + 2] * inv, u[8 * c + 3] * inv);
-        x.z = pack_bf16(u[8 * c + 4] * inv, u[8 * c + 5] * inv);
-        x.w = pack_bf16(u[8 * c + 6] * inv, u[8 * c + 7] * inv);
-        dst[4 + c] = x;
+              for (int i = 0; i < 32; ++i)
+                if (c * 32 + i >= kvalid) v[i] = -INFINITY;
+            }
+          };
+          float va[32], vb[32];
+          // pass 1: exact row max of the tile (S stays in TMEM; two chunks in flight)
+          float mx;
+          {
+            tmem_ld32(s_addr, va);
+            if (nch > 1) tmem_ld32(s_addr + 32, vb);
+            tmem_ld_wait_dep(va);
+            if (nch > 1) tmem_ld_wait_dep(vb);
+            mask(0, va);
+            mx = chunk_max_log2(va, scale_log2);
+            if (nch > 1) {
+              mask(1, vb);
+              mx = fmaxf(mx, chunk_max_log2(vb, scale_log2));
+            }
+            if (nch > 2) {
+              tmem_ld32(s_addr + 64, va);
+              if (nch > 3) tmem_ld32(s_addr + 96, vb);
+              tmem_ld_wait_dep(va);
+              if (nch > 3) tmem_ld_wait_dep(vb);
+              mask(2, va);
+              mx = fmaxf(mx, chunk_max_log2(va, scale_log2));
+              if (nch > 3) {
+                mask(3, vb);
+                mx = fmaxf(mx, chunk_max_log2(vb, scale_log2));
+              }
+            }
+          }
+          // the exponent offset m_used only moves when a row max exceeds it by > 8 (p <= 256),
+          // so O is rescaled in TMEM about once per row
+          const bool raise = mx > m_used + 8.f;
+          const bool rescale = __any_sync(0xffffffffu, raise);
+          float alpha = 1.f;
+          if (rescale) {
+            const float m_new = fmaxf(m_used, mx);
+            alpha = fast_exp2(m_used - m_new);  // 0 on the first tile (m_used = -inf)
+            l *= alpha;
+            m_used = m_new;
+          }
+          // P_x(j-1) must have been consumed (and O_x settled) before P_x(j) / the O rescale
+          if (npv > 0) {
+            mbar_wait(&o_done[x], (npv - 1) & 1);
+            tc_fence_after();
+          }
+          if (tr) ATT_TRACE(tbase, tn, 12);
+          // pass 2: p = 2^(s*scale - m_used) chunk by chunk, next chunk in flight
+          uint64_t lt = 0;  // f32x2 partial row sums
+          tmem_ld32(s_addr, va);
+          tmem_ld_wait_dep(va);
+          if (nch == 1) release_s();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float(&cur)[32] = (c & 1) ? vb : va;
+            float(&nxt)[32] = (c & 1) ? va : vb;
+            if (c + 1 < nch) tmem_ld32(s_addr + (c + 1) * 32, nxt);
+            if (c < nch) {
+              mask(c, cur);
+              lt = fadd2(lt, emit_chunk<POLY>(cur, scale_log2, m_used, p_addr + c * 16, c * 32 + 32 <= kvalid));
+            } else {
+              uint32_t pk[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pk[i] = 0u;
+              tmem_st16u(p_addr + c * 16, pk);
+            }
+            if (c + 1 < nch) {
+              tmem_ld_wait_dep(nxt);
+              if (c + 2 == nch) release_s();
+            }
+          }
+          if (rescale && j > 0) {  // O_x *= alpha in TMEM (warp-collective; alpha = 1 on unchanged rows)
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+              float t[32];
+              tmem_ld32(o_addr + c * 32, t);
+              tmem_ld_wait_dep(t);
+#pragma unroll
+              for (int i = 0; i < 32; ++i) t[i] *= alpha;
+              tmem_st32(o_addr + c * 32, t);
+            }
+          }
+          float l0, l1;
+          f2_unpack(lt, l0, l1);
+          l += l0 + l1;
+          tmem_st_wait();
+        } else {
+          release_s();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (tr) ATT_TRACE(tbase, tn, 13);
+        if (lane == 0) mbar_arrive(&p_full[x]);  // P_x(j) in TMEM
       }
+      // epilogue: O_x / l -> ctx rows
+      mbar_wait(&o_done[x], (npv - 1) & 1);
+      tc_fence_after();
+      if (warp_active) {
+        float t[32], t2[32];
+        tmem_ld32(o_addr, t);
+        tmem_ld32(o_addr + 32, t2);
+        tmem_ld_wait();
+        const int qi = q0 + r;
+        if (qi < T) {
+          const float inv = kTruncScale / l;
+          uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(w.b * T + qi) * D + w.h * 64);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint4 a;
+            a.x = pack_bf16(t[8 * c + 0] * inv, t[8 * c + 1] * inv);
+            a.y = pack_bf16(t[8 * c + 2] * inv, t[8 * c + 3] * inv);
+            a.z = pack_bf16(t[8 * c + 4] * inv, t[8 * c + 5] * inv);
+            a.w = pack_bf16(t[8 * c + 6] * inv, t[8 * c + 7] * inv);
+            dst[c] = a;
+            uint4 b2;
+            b2.x = pack_bf16(t2[8 * c + 0] * inv, t2[8 * c + 1] * inv);
+            b2.y = pack_bf16(t2[8 * c + 2] * inv, t2[8 * c + 3] * inv);
+            b2.z = pack_bf16(t2[8 * c + 4] * inv, t2[8 * c + 5] * inv);
+            b2.w = pack_bf16(t2[8 * c + 6] * inv, t2[8 * c + 7] * inv);
+            dst[4 + c] = b2;
+          }
+        }
+      }
+      tc_fence_before();
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, TMEM_COLS);
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -260,19 +541,42 @@ int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, in
   a->T = T;
   a->D = D;
   a->heads = heads;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int units = B * heads * ((T + 255) / 256);
+  a->grid = units < sms ? units : sms;
+  const char* e = getenv("VPE_ATT_GRID");  // experiment: "all" = one unit per CTA (no persistence)
+  if (e && e[0] == 'a') a->grid = units;
   return VPE_OK;
 }
 
 int launch_attention(const AttnPlan& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
-    attr = true;
+  static int poly = -1;
+  if (poly < 0) {
+    const char* e = getenv("VPE_ATT_POLY");
+    poly = e ? atoi(e) : 3;  // 4 of 16 pairs on the FMA pipe (tools/ubench/emit.cu: best MUFU/FMA balance)
+    cudaFuncSetAttribute(attention_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
+    cudaFuncSetAttribute(attention_tc_kernel<0x0707>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
+    cudaFuncSetAttribute(attention_tc_kernel<0x0303>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
+    cudaFuncSetAttribute(attention_tc_kernel<0x1111>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
   }
-  dim3 grid((a.T + 127) / 128, a.heads, a.B);
   const float scale_log2 = 0.125f * 1.4426950408889634f;
-  attention_tc_kernel<<<grid, 192, SMEM_ATT, s>>>(a.tqkv, a.out, a.T, a.D, scale_log2);
+  if (g_att_trace_on < 0) {
+    const char* e = getenv("VPE_ATT_TRACE");
+    g_att_trace_on = (e && e[0] == '1') ? 1 : 0;
+  }
+  auto k = poly == 0 ? attention_tc_kernel<0>
+                     : (poly == 2 ? attention_tc_kernel<0x0303>
+                                  : (poly == 3 ? attention_tc_kernel<0x1111> : attention_tc_kernel<0x0707>));
+  k<<<a.grid, ATT_THREADS, SMEM_ATT, s>>>(a.tqkv, a.out, a.B, a.T, a.D, a.heads, scale_log2, g_att_trace_on);
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
 }
 
 }  // namespace vpe
+
+extern "C" int vpe_debug_att_trace(unsigned long long* host, int n) {
+  if (!host || n < 0 || n > 4096) return VPE_E_VALUE;
+  VPE_CUDA_TRY(cudaMemcpyFromSymbol(host, vpe::g_att_trace, n * sizeof(unsigned long long)));
+  return VPE_OK;
+}

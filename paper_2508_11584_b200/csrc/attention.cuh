@@ -10,6 +10,7 @@ struct AttnPlan {
   CUtensorMap tqkv;
   __nv_bfloat16* out;
   int B, T, D, heads;
+  int grid;  // persistent CTAs (<= #SMs)
 };
 // qkv: [B*T, 3D] bf16 (q | k | v column blocks, head-major inside each); out: [B*T, D] bf16
 int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, int B, int T, int D, int heads);

@@ -11,6 +11,7 @@
 // (cp.reduce.async.bulk .add.f32), so the SM never reads the residual stream.
 #include <cudaTypedefs.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "gemm.cuh"
@@ -693,7 +694,13 @@ static void finish_grid(GemmPlan* g, int N, int bn, int m_tiles) {
   g->p.n_tiles = (N + bn - 1) / bn;
   g->p.m_tiles = m_tiles;
   const int tiles = g->p.n_tiles * m_tiles;
-  const int ctas = tiles < num_sms() ? tiles : num_sms();
+  int ctas = tiles < num_sms() ? tiles : num_sms();
+  static int mult = -1;  // experiment: VPE_GEMM_GRID=k -> k CTAs per SM worth of grid (tiles spread)
+  if (mult < 0) {
+    const char* e = getenv("VPE_GEMM_GRID");
+    mult = e ? atoi(e) : 1;
+  }
+  if (mult > 1) ctas = tiles < num_sms() * mult ? tiles : num_sms() * mult;
   g->grid = dim3(ctas, 1, 1);
 }
 

@@ -31,7 +31,8 @@ def main():
     args = p.parse_args()
     dev = torch.device("cuda")
     res = []
-    for (M, N, K) in [(16400, 1536, 384), (16400, 384, 1536), (16400, 1152, 384), (8192, 8192, 8192)]:
+    gemms = [] if args.only == "attention" else None
+    for (M, N, K) in [(16400, 1536, 384), (16400, 384, 1536), (16400, 1152, 384), (8192, 8192, 8192)] if gemms is None else gemms:
         a = torch.randn(M, K, device=dev).to(torch.bfloat16)
         w = (torch.randn(N, K, device=dev) * 0.02).to(torch.bfloat16)
         bias = torch.zeros(N, device=dev)
@@ -45,7 +46,7 @@ def main():
                 print(json.dumps(res[-1]), flush=True)
         us = timeit(lambda: torch.matmul(a, w.t(), out=out))
         print(json.dumps(dict(M=M, N=N, K=K, impl="cublas", us=us, tflops=2 * M * N * K / us * 1e-6)), flush=True)
-    for (B, T, H) in [(16, 1025, 6), (1, 1025, 6)]:
+    for (B, T, H) in [(16, 1025, 6), (1, 1025, 6), (8, 1370, 16), (1, 1370, 12)]:
         D = H * 64
         qkv = torch.randn(B * T, 3 * D, device=dev).to(torch.bfloat16)
         us = timeit(lambda: _ops.attention(qkv, B, T, D, H))
