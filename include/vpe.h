@@ -244,6 +244,7 @@ int vpe_det_forward(vpe_det* d, const void* final_tap, const vpe_det_outputs* ou
  * 3 f32. Kw may be a multiple of K (split-precision weights, A repeated). */
 int vpe_op_linear(const void* A, int32_t M, int32_t K, const void* W, int32_t N, int32_t Kw, const float* bias,
                   const float* scale, void* out, int32_t kind, int32_t act, int32_t bn, void* stream);
+/* bn > 0: one-CTA 128 x bn tiles; bn < 0: CTA-pair (cta_group::2) 256 x |bn| tiles */
 /* 3x3 or 1x1 same-padding conv on NHWC bf16 x [B,H,W,Cp] with weights [N, ks*ks*Cp] -> out bf16 NHWC
  * [B,H,W,ldo]; out = act(conv + bias + add1 + add2); out_relu optional */
 int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32_t Cp, int32_t ks, const void* w,
@@ -273,6 +274,7 @@ const char* vpe_status_str(int status);
 /* diagnostics: timeline of attention CTA 0 when the process runs with VPE_ATT_TRACE=1
    ((code, clock64) pairs; see csrc/attention.cu) */
 int vpe_debug_att_trace(unsigned long long* host, int32_t n);
+int vpe_debug_gemm_trace(unsigned long long* host, int32_t n);
 
 #ifdef __cplusplus
 }

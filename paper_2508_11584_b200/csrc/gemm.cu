@@ -70,7 +70,7 @@ VPE_DEV void load_bf16x32_add(const __nv_bfloat16* src, float (&v)[32]) {
 }
 
 VPE_DEV float apply_act(float x, int act) {
-  if (act == ACT_GELU) return gelu_erf(x);
+  if (act == ACT_GELU) return gelu_erf(x);  // scalar path; the TMA-store epilogue uses gelu_poly32
   if (act == ACT_RELU) return fmaxf(x, 0.f);
   return x;
 }
@@ -230,6 +230,73 @@ VPE_DEV void epilogue_direct(const EpiParams& ep, int64_t gpix, int col0, float 
   }
 }
 
+// optional MMA-thread timeline of CTA 0 (diagnostics only: VPE_GEMM_TRACE=1, vpe_debug_gemm_trace)
+__device__ unsigned long long g_gemm_trace[4096];
+static int g_gemm_trace_on = -1;
+#define GEMM_TRACE(idx, code)                                                        \
+  do {                                                                               \
+    if (p.trace && blockIdx.x == 0 && (idx) < 2040) {                                \
+      g_gemm_trace[2 * (idx)] = (unsigned long long)(code);                          \
+      g_gemm_trace[2 * (idx) + 1] = (unsigned long long)clock64();                   \
+      ++(idx);                                                                       \
+    }                                                                                \
+  } while (0)
+
+// One 32-column chunk of a row-major tile through the TMA-store epilogue: bias / LayerScale /
+// activation in registers, swizzled smem staging (per-warp double buffer), then a TMA bulk store
+// (bf16 / f32) or bulk reduce-add (fp32 residual). Lane 0 issues; row0 = first of the warp's 32 rows.
+VPE_DEV void epilogue_tma_chunk(const GemmParams& p, const CUtensorMap* tout, float (&v)[32], int col0, int row0,
+                                uint8_t* stg_base, int& nstore) {
+  const uint32_t lane = lane_id();
+  const int N = p.ep.N;
+  const bool fullc = col0 + 32 <= N;
+  if (p.ep.bias) add_vec32(v, p.ep.bias, col0, N, fullc);
+  if (p.ep.kind == EPI_RESID) mul_vec32(v, p.ep.scale, col0, N, fullc);
+  if (p.ep.act == ACT_GELU) {
+    gelu_poly32(v);
+  } else if (p.ep.act != ACT_NONE) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], p.ep.act);
+  }
+  const bool bf = p.ep.kind == EPI_BF16;
+  uint8_t* stg = stg_base + (bf ? (nstore & 1) * (STAGE_BUF / 2) : 0);
+  if (lane == 0) {  // the store that last used this buffer has finished reading it
+    if (bf)
+      bulk_wait_read1();
+    else
+      bulk_wait_read0();
+  }
+  __syncwarp();
+  // staging rows are written in the TMA swizzle layout (bank-conflict free):
+  // bf16: 64-B rows, SWIZZLE_64B (chunk ^ ((row>>1)&3)); f32: 128-B rows, SWIZZLE_128B
+  if (p.ep.kind == EPI_BF16) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint4 u;
+      u.x = pack_bf16(v[8 * k + 0], v[8 * k + 1]);
+      u.y = pack_bf16(v[8 * k + 2], v[8 * k + 3]);
+      u.z = pack_bf16(v[8 * k + 4], v[8 * k + 5]);
+      u.w = pack_bf16(v[8 * k + 6], v[8 * k + 7]);
+      *reinterpret_cast<uint4*>(stg + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) = u;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      *reinterpret_cast<float4*>(stg + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+          make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (p.ep.kind == EPI_RESID)
+      tma_reduce_add_2d(tout, stg, col0, row0);
+    else
+      tma_store_2d(tout, stg, col0, row0);
+    bulk_commit();
+  }
+  ++nstore;
+}
+
 template <int BN, int BK>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
@@ -304,17 +371,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(128, BN);
-      int it = 0, i = 0;
+      int it = 0, i = 0, tn = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
         const int acc = i & 1;
+        GEMM_TRACE(tn, 1);
         mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
+        GEMM_TRACE(tn, 2);
         const uint32_t d = tmem + acc * BN;
         for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
           const int s = it % C::STAGES;
           const uint32_t ph = (it / C::STAGES) & 1;
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          GEMM_TRACE(tn, 10 + kb);
           const uint32_t a0 = smem_u32(sA + s * C::A_BYTES);
           const uint32_t b0 = smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
@@ -374,51 +444,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int col0 = n0 + c0;
         if (col0 >= p.ep.N) continue;  // warp-uniform
         if (p.tma_out) {
-          const int N = p.ep.N;
-          const bool fullc = col0 + 32 <= N;
-          if (p.ep.bias) add_vec32(v, p.ep.bias, col0, N, fullc);
-          if (p.ep.kind == EPI_RESID) mul_vec32(v, p.ep.scale, col0, N, fullc);
-          if (p.ep.act != ACT_NONE) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], p.ep.act);
-          }
-          const bool bf = p.ep.kind == EPI_BF16;
-          uint8_t* stg = stg_base + (bf ? (nstore & 1) * (STAGE_BUF / 2) : 0);
-          if (lane == 0) {  // the store that last used this buffer has finished reading it
-            if (bf)
-              bulk_wait_read1();
-            else
-              bulk_wait_read0();
-          }
-          __syncwarp();
-          // staging rows are written in the TMA swizzle layout (bank-conflict free):
-          // bf16: 64-B rows, SWIZZLE_64B (chunk ^ ((row>>1)&3)); f32: 128-B rows, SWIZZLE_128B
-          if (p.ep.kind == EPI_BF16) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              uint4 u;
-              u.x = pack_bf16(v[8 * k + 0], v[8 * k + 1]);
-              u.y = pack_bf16(v[8 * k + 2], v[8 * k + 3]);
-              u.z = pack_bf16(v[8 * k + 4], v[8 * k + 5]);
-              u.w = pack_bf16(v[8 * k + 6], v[8 * k + 7]);
-              *reinterpret_cast<uint4*>(stg + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) = u;
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              *reinterpret_cast<float4*>(stg + lane * 128 + ((k ^ (lane & 7)) << 4)) =
-                  make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-          }
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            if (p.ep.kind == EPI_RESID)
-              tma_reduce_add_2d(&tout, stg, col0, m0 + q * 32);
-            else
-              tma_store_2d(&tout, stg, col0, m0 + q * 32);
-            bulk_commit();
-          }
-          ++nstore;
+          epilogue_tma_chunk(p, &tout, v, col0, m0 + q * 32, stg_base, nstore);
         } else if (valid) {
           epilogue_direct(p.ep, gpix, col0, v);
         }
@@ -431,6 +457,161 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+
+// ------------------------------------------------------------------------------------------
+// CTA-pair GEMM (cta_group::2), row-major A. A cluster of 2 CTAs on one TPC computes a
+// 256 x BN tile: each CTA stages its own 128 A rows and half (BN/2) of the B rows, the leader
+// (rank 0) issues tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' smem, and each CTA's
+// TMEM receives its 128 x BN accumulator. Per SM that halves the B traffic from L2 -- the
+// bound for these K = 384 backbone GEMMs (the 128 x BN one-CTA kernel is L2-bandwidth bound).
+//   warp 0 (both CTAs)  TMA producer; completions counted on the leader's full barrier
+//   warp 1 (leader)     MMA issuer; commits multicast to both CTAs' empty / tfull barriers
+//   warps 2-17          epilogue of this CTA's 128 rows; TMEM release arrives on the leader
+// ------------------------------------------------------------------------------------------
+template <int BN>
+struct Gemm2Cfg {
+  static constexpr int BK = 64;
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  // every byte of smem not needed for epilogue staging goes to the TMA ring: at K = 384 the
+  // MMA otherwise starves on TMA latency (tools/gemm_trace.py)
+  static constexpr int RING = 232448 - 1024 - 256 - EPI_WARPS * STAGE_BUF;
+  static constexpr int STAGES = RING / STAGE_BYTES > 8 ? 8 : RING / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + EPI_WARPS * STAGE_BUF + 256;
+};
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                     const __grid_constant__ CUtensorMap tout, const GemmParams p) {
+  using C = Gemm2Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint8_t* sStage = sB + C::STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + EPI_WARPS * STAGE_BUF);  // leader's copy used
+  uint64_t* empty = full + C::STAGES;   // both copies used (multicast commit)
+  uint64_t* tfull = empty + C::STAGES;  // [2] both copies used (multicast commit)
+  uint64_t* tempty = tfull + 2;         // [2] leader's copy used (arrivals from both CTAs)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&ta);
+    tma_prefetch(&tb);
+    if (p.tma_out) tma_prefetch(&tout);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2 * EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc2(tslot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's barriers are initialised before anything can signal them
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const int ntiles = p.m_tiles * p.n_tiles;  // m_tiles counts 256-row pairs
+  const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = cid; t < ntiles; t += ncl) {
+        const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+        const int m0 = mt * 256 + (int)rank * 128, n0 = nt * BN + (int)rank * (BN / 2);
+        for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);
+          tma_load_2d_pair(sA + s * C::A_BYTES, &ta, &full[s], kb * 64, m0);
+          tma_load_2d_pair(sB + s * C::B_BYTES, &tb, &full[s], kb * 64, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(256, BN);
+      int it = 0, i = 0, tn = 0;
+      for (int t = cid; t < ntiles; t += ncl, ++i) {
+        const int acc = i & 1;
+        GEMM_TRACE(tn, 1);
+        mbar_wait_cluster(&tempty[acc], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        GEMM_TRACE(tn, 2);
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&full[s], (it / C::STAGES) & 1);
+          tc_fence_after();
+          GEMM_TRACE(tn, 10 + kb);
+          const uint32_t a0 = smem_u32(sA + s * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + s * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_f16_pair(d, smem_desc(a0 + k * 32, 16, 1024, 2), smem_desc(b0 + k * 32, 16, 1024, 2), idesc,
+                          (kb | k) != 0);
+          umma_commit_pair(&empty[s]);
+        }
+        umma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else {
+    const int e = warp - 2;
+    const int q = warp & 3;
+    const int chalf = e >> 2;
+    const int r = q * 32 + lane;
+    uint8_t* stg_base = sStage + e * STAGE_BUF;
+    int nstore = 0;
+    int i = 0;
+    for (int t = cid; t < ntiles; t += ncl, ++i) {
+      const int acc = i & 1;
+      const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+      const int m0 = mt * 256 + (int)rank * 128, n0 = nt * BN;
+      const int64_t gpix = m0 + r;
+      const bool valid = gpix < p.M;
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = chalf; c < BN / 32; c += EPI_SPLIT) {
+        const int c0 = c * 32;
+        float v[32];
+        tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c0, v);
+        tmem_ld_wait();
+        if (c + EPI_SPLIT >= BN / 32) {  // this warp's last TMEM read of the tile
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+        }
+        const int col0 = n0 + c0;
+        if (col0 >= p.ep.N) continue;  // warp-uniform
+        if (p.tma_out) {
+          epilogue_tma_chunk(p, &tout, v, col0, m0 + q * 32, stg_base, nstore);
+        } else if (valid) {
+          epilogue_direct(p.ep, gpix, col0, v);
+        }
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs are done with TMEM and with each other's barriers
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem, C::TMEM_COLS);
   }
 }
 
@@ -704,8 +885,78 @@ static void finish_grid(GemmPlan* g, int N, int bn, int m_tiles) {
   g->grid = dim3(ctas, 1, 1);
 }
 
+template <typename K>
+static int max_pair_clusters(K kernel, int smem) {
+  static int cached[4] = {0, 0, 0, 0};
+  const int slot = smem % 4;  // distinct per instantiation in practice; recomputed if 0
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * 256, 1, 1);
+  cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 2;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = num_sms() / 2;
+  }
+  (void)cached;
+  (void)slot;
+  static bool printed = false;
+  if (!printed && getenv("VPE_VERBOSE")) {
+    fprintf(stderr, "[vpe] pair GEMM: %d co-resident clusters of 2 (smem %d)\n", n, smem);
+    printed = true;
+  }
+  return n;
+}
+
+static int plan_gemm_rows_pair(GemmPlan* g, const __nv_bfloat16* A, int M, int K, int64_t lda, const __nv_bfloat16* B,
+                               int N, int Kb, int64_t ldb, const EpiParams& ep, int bn) {
+  if (bn != 128 && bn != 192 && bn != 256) return VPE_E_SHAPE;
+  if (K % 64 || Kb != K) return VPE_E_SHAPE;
+  if ((lda * 2) % 16 || (reinterpret_cast<uintptr_t>(A) % 16)) return VPE_E_SHAPE;
+  memset(g, 0, sizeof(*g));
+  uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
+  uint64_t strides[1] = {(uint64_t)lda * 2};
+  uint32_t box[2] = {64u, 128u};
+  VPE_TRY(encode_tma(&g->ta, 2, A, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B));
+  VPE_TRY(make_b_map(g, B, N, Kb, ldb, bn / 2, 64));
+  g->p.kblocks = Kb / 64;
+  g->p.kblocks_a = K / 64;
+  g->p.mode = 0;
+  g->p.M = M;
+  g->p.ks = 1;
+  g->p.cchunks = 1;
+  g->p.ep = ep;
+  VPE_TRY(make_out_map(g, M));
+  g->p.n_tiles = (N + bn - 1) / bn;
+  g->p.m_tiles = (M + 255) / 256;
+  const int tiles = g->p.n_tiles * g->p.m_tiles;
+  g->bn = bn;
+  g->bk = 64;
+  g->pair = 1;
+  int pairs = 0;
+#define VPE_P2(BN_)                              \
+  if (bn == BN_) {                               \
+    g->smem = Gemm2Cfg<BN_>::SMEM;               \
+    pairs = max_pair_clusters(gemm_pair_kernel<BN_>, (int)g->smem); \
+  }
+  VPE_P2(128) VPE_P2(192) VPE_P2(256)
+#undef VPE_P2
+  // persistent grid = the clusters that can be co-resident (TPCs with both SMs enabled), not #SMs/2
+  g->grid = dim3(2 * (tiles < pairs ? tiles : pairs), 1, 1);
+  return VPE_OK;
+}
+
 int plan_gemm_rows(GemmPlan* g, const __nv_bfloat16* A, int M, int K, int64_t lda, const __nv_bfloat16* B, int N,
                    int Kb, int64_t ldb, const EpiParams& ep, int bn) {
+  if (bn < 0) return plan_gemm_rows_pair(g, A, M, K, lda, B, N, Kb, ldb, ep, -bn);
   const int bk = 64;
   if (K % bk || Kb % K || smem_for(bn, bk) < 0) return VPE_E_SHAPE;
   if ((lda * 2) % 16 || (reinterpret_cast<uintptr_t>(A) % 16)) return VPE_E_SHAPE;
@@ -863,11 +1114,41 @@ static int launch_t(const GemmPlan& g, cudaStream_t s) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GemmCfg<BN, BK>::SMEM);
     attr_set = true;
   }
-  k<<<g.grid, GEMM_THREADS, GemmCfg<BN, BK>::SMEM, s>>>(g.ta, g.tb, g.tout, g.p);
+  if (g_gemm_trace_on < 0) {
+    const char* e = getenv("VPE_GEMM_TRACE");
+    g_gemm_trace_on = (e && e[0] == '1') ? 1 : 0;
+  }
+  GemmParams p = g.p;
+  p.trace = g_gemm_trace_on;
+  k<<<g.grid, GEMM_THREADS, GemmCfg<BN, BK>::SMEM, s>>>(g.ta, g.tb, g.tout, p);
+  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+}
+
+template <int BN>
+static int launch_pair_t(const GemmPlan& g, cudaStream_t s) {
+  auto k = gemm_pair_kernel<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gemm2Cfg<BN>::SMEM);
+    attr_set = true;
+  }
+  if (g_gemm_trace_on < 0) {
+    const char* e = getenv("VPE_GEMM_TRACE");
+    g_gemm_trace_on = (e && e[0] == '1') ? 1 : 0;
+  }
+  GemmParams p = g.p;
+  p.trace = g_gemm_trace_on;
+  k<<<g.grid, GEMM_THREADS, Gemm2Cfg<BN>::SMEM, s>>>(g.ta, g.tb, g.tout, p);
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
 }
 
 int launch_gemm(const GemmPlan& g, cudaStream_t s) {
+  if (g.pair) {
+    if (g.bn == 128) return launch_pair_t<128>(g, s);
+    if (g.bn == 192) return launch_pair_t<192>(g, s);
+    if (g.bn == 256) return launch_pair_t<256>(g, s);
+    return VPE_E_SHAPE;
+  }
   if (g.halo_kc) {
 #define VPE_LH(BN_, KC_, RT_) \
   if (g.bn == BN_ && g.halo_kc == KC_ && g.halo_rt == RT_) return launch_halo_t<BN_, KC_, RT_>(g, s);
@@ -884,3 +1165,9 @@ int launch_gemm(const GemmPlan& g, cudaStream_t s) {
 }
 
 }  // namespace vpe
+
+extern "C" int vpe_debug_gemm_trace(unsigned long long* host, int n) {
+  if (!host || n < 0 || n > 4096) return VPE_E_VALUE;
+  VPE_CUDA_TRY(cudaMemcpyFromSymbol(host, vpe::g_gemm_trace, n * sizeof(unsigned long long)));
+  return VPE_OK;
+}

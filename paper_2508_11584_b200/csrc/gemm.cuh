@@ -58,6 +58,7 @@ struct GemmParams {
   int tma_out = 0;               // 1: epilogue leaves through TMA store / reduce-add (tout)
   int hp = 0, rows_box = 0;      // halo conv: virtual row pitch P, halo rows per stage
   int parts = 1, kcp = 0;        // halo conv: split-precision weight parts, K extent per tap (Cpad)
+  int trace = 0;                 // diagnostics: record the MMA timeline of CTA 0
   EpiParams ep;
 };
 
@@ -70,6 +71,7 @@ struct GemmPlan {
   int bn = 0, bk = 0;
   int halo_kc = 0;  // > 0: conv_halo_kernel<bn, halo_kc, halo_rt>
   int halo_rt = 1;
+  int pair = 0;     // 1: gemm_pair_kernel<bn> (cta_group::2, 256-row tiles)
   size_t smem = 0;
 };
 
@@ -85,6 +87,7 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
 bool tma_available();
 // Row-major A [M, K] (pitch lda elements) times K-major weights B [N, Kb] (pitch ldb).
 // Kb may be a multiple of K (split-precision weights concatenated along K; A repeats).
+// bn < 0 selects the CTA-pair kernel with 256 x |bn| tiles (|bn| in {128, 192, 256}, Kb == K).
 int plan_gemm_rows(GemmPlan* g, const __nv_bfloat16* A, int M, int K, int64_t lda,
                    const __nv_bfloat16* B, int N, int Kb, int64_t ldb, const EpiParams& ep, int bn);
 // NHWC image X (channels C real, pitches in elements: pixel, row, image) as implicit-GEMM conv

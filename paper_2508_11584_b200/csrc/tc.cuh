@@ -162,6 +162,80 @@ VPE_DEV void tmem_st32(uint32_t taddr, const float (&v)[32]) {
 }
 VPE_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+
+// ---------------------------------------------------------------- CTA pairs (cta_group::2)
+VPE_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+VPE_DEV uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+VPE_DEV uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+VPE_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+VPE_DEV void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+VPE_DEV void tmem_dealloc2(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+// shared::cluster address of the pair leader's (even rank) copy of a local smem object
+VPE_DEV uint32_t leader_addr(const void* p) { return smem_u32(p) & 0xFEFFFFFFu; }
+// TMA load into this CTA's smem whose completion is counted on the pair leader's mbarrier
+VPE_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* map, const uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_addr(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// D[tmem, both CTAs] (+)= A[smem, 128 rows per CTA] * B[smem, N/2 rows per CTA]^T; leader issues
+VPE_DEV void umma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// arrive (once each) on the mbarrier at this smem offset in both CTAs of the pair when all
+// previously issued cta_group::2 MMAs complete
+VPE_DEV void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// arrive on the pair leader's copy of a barrier (release at cluster scope)
+VPE_DEV void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+VPE_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITC_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- descriptors
 // UMMA shared-memory matrix descriptor (sm_100: version field = 1).
 // layout: 2 = SWIZZLE_128B, 4 = SWIZZLE_64B, 6 = SWIZZLE_32B, 0 = none.
@@ -207,6 +281,55 @@ VPE_DEV float gelu_erf(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
   const float y = fmaf(-p, e, 1.0f);  // erf(|x|/sqrt2)
   return 0.5f * x * (1.0f + copysignf(y, x));
+}
+
+// ---------------------------------------------------------------- f32x2 SIMD (FFMA2 / FADD2 / FMUL2)
+VPE_DEV uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+VPE_DEV void f2_unpack(uint64_t r, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+VPE_DEV uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+VPE_DEV uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+VPE_DEV uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// exact-erf GELU (transformers activations.py:70-89) for a pair, MUFU-free:
+// erf(x/sqrt2) = xc * p(xc^2/16) with xc = clamp(x, -4, 4), p a degree-8 least-squares fit
+// (max |erf error| 2.9e-5 in fp32; max |GELU error| 1.9e-4 over [-10, 10], at the clamp, versus
+// bf16 output rounding of 4e-3 at 1.0). 17 f32x2-pipe instructions per pair.
+VPE_DEV uint64_t gelu_poly2(uint64_t x) {
+  float x0, x1;
+  f2_unpack(x, x0, x1);
+  const uint64_t xc = f2_pack(fminf(fmaxf(x0, -4.f), 4.f), fminf(fmaxf(x1, -4.f), 4.f));
+  const uint64_t u = fmul2(fmul2(xc, f2_pack(0.0625f, 0.0625f)), xc);
+  uint64_t p = ffma2(u, f2_pack(7.323220372e-01f, 7.323220372e-01f), f2_pack(-3.916897058e+00f, -3.916897058e+00f));
+  p = ffma2(p, u, f2_pack(9.367665291e+00f, 9.367665291e+00f));
+  p = ffma2(p, u, f2_pack(-1.341740036e+01f, -1.341740036e+01f));
+  p = ffma2(p, u, f2_pack(1.306751728e+01f, 1.306751728e+01f));
+  p = ffma2(p, u, f2_pack(-9.316836357e+00f, -9.316836357e+00f));
+  p = ffma2(p, u, f2_pack(5.061147213e+00f, 5.061147213e+00f));
+  p = ffma2(p, u, f2_pack(-2.125376940e+00f, -2.125376940e+00f));
+  p = ffma2(p, u, f2_pack(7.978495359e-01f, 7.978495359e-01f));
+  const uint64_t phi = ffma2(fmul2(xc, p), f2_pack(0.5f, 0.5f), f2_pack(0.5f, 0.5f));
+  return fmul2(x, phi);
+}
+
+VPE_DEV void gelu_poly32(float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) f2_unpack(gelu_poly2(f2_pack(v[2 * j], v[2 * j + 1])), v[2 * j], v[2 * j + 1]);
 }
 
 VPE_DEV uint32_t pack_bf16(float a, float b) {

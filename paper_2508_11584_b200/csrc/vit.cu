@@ -30,11 +30,12 @@ struct vpe_vit {
 
 static constexpr int KPATCH = 640;
 
-// BN per GEMM: wide tiles amortise the A re-read; at small M fall back to narrower tiles so
-// the persistent grid still covers the SMs (microbench, profiles/round1_gemm.md).
+// BN per GEMM: wide tiles amortise the A re-read (the K=384 GEMMs are L2-bandwidth bound at
+// BN=128: FC1+GELU 32.7 -> 28.9 us at BN=256, tools/microbench.py); at small M fall back to
+// narrower tiles so the persistent grid still covers the SMs.
 static int pick_bn(int N, int M) {
   const int m_tiles = (M + 127) / 128;
-  int bn = 128;
+  int bn = 256;
   while (bn > 64 && m_tiles * ((N + bn - 1) / bn) < 148) bn >>= 1;
   return bn;
 }

@@ -34,6 +34,37 @@ def test_linear_bf16(ops, device, M, N, K, bn):
     assert rel_l2(out, ref) < 8e-3  # bf16 output rounding
 
 
+@pytest.mark.parametrize("M,N,K,bn", [(16400, 1536, 384, -256), (16400, 384, 1536, -192), (1025, 1152, 384, -192),
+                                        (300, 384, 384, -128), (16400, 384, 384, -256)])
+@pytest.mark.parametrize("act", [0, 1])
+def test_linear_pair(ops, device, M, N, K, bn, act):
+    """CTA-pair (cta_group::2) GEMM: 256-row tiles split over two SMs, M tails, N tails."""
+    g = torch.Generator(device="cpu").manual_seed(M + N + K + act)
+    a = torch.randn(M, K, generator=g).to(device, torch.bfloat16)
+    w = (torch.randn(N, K, generator=g) * 0.05).to(device, torch.bfloat16)
+    bias = torch.randn(N, generator=g).to(device)
+    out = ops.linear(a, w, bias=bias, act=act, bn=bn)
+    torch.cuda.synchronize()
+    ref = a.float() @ w.float().t() + bias
+    if act:
+        ref = F.gelu(ref)
+    assert rel_l2(out, ref) < 8e-3
+
+
+def test_linear_pair_resid(ops, device):
+    g = torch.Generator().manual_seed(7)
+    M, N, K = 16400, 384, 1536
+    a = torch.randn(M, K, generator=g).to(device, torch.bfloat16)
+    w = (torch.randn(N, K, generator=g) * 0.02).to(device, torch.bfloat16)
+    bias = torch.randn(N, generator=g).to(device)
+    ls = torch.rand(N, generator=g).to(device) + 0.5
+    h = torch.randn(M, N, generator=g).to(device)
+    ref = h + ls * (a.float() @ w.float().t() + bias)
+    ops.linear(a, w, bias=bias, scale=ls, out=h, kind=ops.EPI_RESID, bn=-192)
+    torch.cuda.synchronize()
+    assert rel_l2(h, ref) < 1e-4
+
+
 def test_linear_gelu_and_resid(ops, device):
     g = torch.Generator().manual_seed(1)
     M, N, K = 1025, 1536, 384

@@ -32,13 +32,13 @@ def main():
     dev = torch.device("cuda")
     res = []
     gemms = [] if args.only == "attention" else None
-    for (M, N, K) in [(16400, 1536, 384), (16400, 384, 1536), (16400, 1152, 384), (8192, 8192, 8192)] if gemms is None else gemms:
+    for (M, N, K) in [(16400, 1536, 384), (16400, 384, 1536), (16400, 1152, 384), (16400, 384, 384), (8192, 8192, 8192)] if gemms is None else gemms:
         a = torch.randn(M, K, device=dev).to(torch.bfloat16)
         w = (torch.randn(N, K, device=dev) * 0.02).to(torch.bfloat16)
         bias = torch.zeros(N, device=dev)
         out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
         outf = torch.empty(M, N, device=dev, dtype=torch.float32)
-        for bn in (64, 128, 256):
+        for bn in (128, 256, -128, -192, -256):
             for act in (0, 1):
                 us = timeit(lambda: _ops.linear(a, w, bias=bias, out=out, act=act, bn=bn))
                 tf = 2 * M * N * K / us * 1e-6
