@@ -453,7 +453,7 @@ extern "C" int vpe_det_forward(vpe_det* d, const void* final_tap, const vpe_det_
     const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(final_tap) + D;
     const int kb = 9 * D;
     if (plan_conv_halo(&d->g, x, B, h, h, D, D, (int64_t)h * D, (int64_t)T * D, 2,
-                       static_cast<const __nv_bfloat16*>(d->w.conv_w_split), D, 2 * kb, ep, 64) != VPE_OK)
+                       static_cast<const __nv_bfloat16*>(d->w.conv_w_split), D, 2 * kb, ep, 128) != VPE_OK)
       VPE_TRY(plan_gemm_conv(&d->g, x, B, h, h, D, D, (int64_t)h * D, (int64_t)T * D, 3, 64,
                              static_cast<const __nv_bfloat16*>(d->w.conv_w_split), D, 2 * kb, 2 * kb, ep, 64));
     d->bound = final_tap;
