@@ -1,0 +1,173 @@
+// Microbenchmark (diagnostics only): a bare TMA -> mbarrier -> tcgen05.mma mainloop (no epilogue)
+// for M128 x N256 x K64 k-blocks, STAGES ring, A/B streamed from an L2-resident buffer.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 0x7) << 61;
+  return d;
+}
+__host__ __device__ constexpr uint32_t idesc(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c)); }
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+  asm volatile("{\n\t.reg .pred P1;\nW%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra W%=;\n\t}" ::"r"(smem_u32(b)), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void tma2(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+               ::"r"(smem_u32(dst)), "l"((uint64_t)m), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+
+template <int STAGES, int BN>
+__global__ void k(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, unsigned long long* out,
+                  int iters, int epi, void* gout, int throttle) {
+  constexpr int AB = 128 * 128, BB = BN * 128, SB = AB + BB;
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* s = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], done;
+  volatile __shared__ int stop_flag;
+  if (threadIdx.x == 0) stop_flag = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0 && lane == 0) {
+    for (int it = 0; it < iters; ++it) {
+      const int st = it % STAGES;
+      mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[st])), "r"(SB) : "memory");
+      const int kb = it % 6, mt = (blockIdx.x + (it / 6) * 148) % 128;
+      tma2(s + st * SB, &ta, &full[st], kb * 64, mt * 128);
+      tma2(s + st * SB + AB, &tb, &full[st], kb * 64, ((it / 6) % 6) * BN);
+    }
+  } else if (warp == 1 && lane == 0) {
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int st = it % STAGES;
+      mbar_wait(&full[st], (it / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a0 = smem_u32(s + st * SB), b0 = a0 + AB;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint64_t ad = desc(a0 + kk * 32, 16, 1024, 2), bd = desc(b0 + kk * 32, 16, 1024, 2);
+        const uint32_t id = idesc(128, BN), acc = ((it % 6) | kk) ? 1u : 0u;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tslot), "l"(ad), "l"(bd), "r"(id), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&done)) : "memory");
+    mbar_wait(&done, 0);
+    out[blockIdx.x] = clock64() - t0;
+    stop_flag = 1;
+  } else if (warp >= 4 && epi == 2) {
+    // fake epilogue: 2 KB bulk stores smem -> global from each warp (TMA store path), 1 in flight
+    if (lane == 0) {
+      char* dst = reinterpret_cast<char*>(gout) + ((size_t)blockIdx.x * 8 + (warp - 4)) * 2048 * 64;
+      const uint32_t src = smem_u32(s);  // any 2 KB of smem
+      int n = 0;
+      while (!stop_flag) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 2048;" ::"l"(dst + (n & 63) * 2048), "r"(src) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        ++n;
+        for (int sp = 0; sp < throttle; ++sp) __nanosleep(32);
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      out[148 + blockIdx.x * 8 + warp - 4] = n;
+    }
+  } else if (warp >= 4 && epi) {
+    // fake epilogue: tcgen05.ld 32x32b.x32 from the OTHER accumulator half (cols 256..511)
+    const uint32_t base = tslot + ((uint32_t)((warp & 3) * 32) << 16) + 256 + ((warp >> 2) - 1) * 64;
+    float acc = 0.f;
+    while (!stop_flag) {
+      uint32_t r[32];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+            "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+            "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+            "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(base));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int i = 0; i < 32; ++i) acc += __uint_as_float(r[i]);
+    }
+    if (acc == 1.2345f) out[0] = 0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tslot));
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 enc;
+static CUtensorMap mk(void* p, uint64_t rows, uint32_t boxrows) {
+  CUtensorMap tm;
+  uint64_t dims[2] = {384, rows};
+  uint64_t strides[1] = {768};
+  uint32_t box[2] = {64, boxrows}, es[2] = {1, 1};
+  enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, p, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return tm;
+}
+
+template <int S, int BN>
+void run(unsigned long long* d, CUtensorMap ta, CUtensorMap tb, int epi = 0, int throttle = 0) {
+  static void* gout = nullptr;
+  if (!gout) cudaMalloc(&gout, 148ull * 8 * 2048 * 64);
+  constexpr int smem = S * (128 * 128 + BN * 128) + 2048;
+  cudaFuncSetAttribute(k<S, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int iters = 3000;
+  unsigned long long h[148 + 148 * 8];
+  k<S, BN><<<148, epi ? 384 : 128, smem>>>(ta, tb, d, iters, epi, gout, throttle);
+  k<S, BN><<<148, epi ? 384 : 128, smem>>>(ta, tb, d, iters, epi, gout, throttle);
+  cudaDeviceSynchronize();
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  unsigned long long mx = 0, sum = 0;
+  for (int i = 0; i < 148; ++i) { mx = h[i] > mx ? h[i] : mx; sum += h[i]; }
+  unsigned long long nst = 0;
+  if (epi == 2) for (int i = 0; i < 148 * 8; ++i) nst += h[148 + i];
+  printf("stores/SM=%.0f (%.1f B/clk/SM)  ", nst / 148.0, nst / 148.0 * 2048 / ((double)sum / 148));
+  printf("epi=%d stages=%d BN=%d  clk/kblock mean=%.1f max=%.1f (ideal %d)  (%s)\n", epi, S, BN, (double)sum / 148 / iters,
+         (double)mx / iters, BN * 2, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+  void *A, *B;
+  cudaMalloc(&A, 16384ull * 768);
+  cudaMalloc(&B, 1536ull * 768);
+  cudaMemset(A, 0, 16384ull * 768);
+  cudaMemset(B, 0, 1536ull * 768);
+  unsigned long long* d;
+  cudaMalloc(&d, (148 + 148 * 8) * 8);
+  CUtensorMap ta = mk(A, 16384, 128), tb = mk(B, 1536, 256), tb128 = mk(B, 1536, 128);
+  run<3, 256>(d, ta, tb);
+  run<4, 256>(d, ta, tb);
+  run<4, 128>(d, ta, tb128);
+  run<6, 128>(d, ta, tb128);
+  run<4, 256>(d, ta, tb, 1);
+  run<4, 256>(d, ta, tb, 2, 0);
+  run<4, 256>(d, ta, tb, 2, 4);
+  run<4, 256>(d, ta, tb, 2, 16);
+  return 0;
+}
