@@ -12,10 +12,11 @@
 //               pulled S_X(j) into registers; O_X += P_X(j) V_j with P read from TMEM (.kind::f16
 //               A-from-TMEM), so P never touches shared memory
 //   warp 3      idle (completes warpgroup 0)
-//   warps 4-7   softmax A, warps 8-11 softmax B: one thread per query row, the whole 128-key S
-//               row in registers; tree max / tree sum; p = 2^(s*scale - m) written to TMEM as
-//               bf16 pairs; O is rescaled in TMEM only when the running max rises by > 8 (log2),
-//               i.e. almost never after the first KV tile.
+//   warps 4-11  softmax A, warps 12-19 softmax B: two warps per 32 query rows, one per 64-key
+//               half of each S tile; the pair agrees on the row max through smem + a named
+//               barrier; p = 2^(s*scale - m) written to TMEM as bf16 pairs; O is rescaled in TMEM
+//               only when the running max rises by > 8 (log2), i.e. almost never after the first
+//               KV tile.
 // TMEM (512 columns): S_A | S_B | P_A | P_B | O_A | O_B.
 // Rows/keys past T (tail tiles) are computed on whatever the TMA brought (the next image's rows
 // or zero fill) and masked: invalid keys get p = 0, invalid rows are never stored, and warps whose
@@ -33,8 +34,9 @@ namespace vpe {
 namespace {
 constexpr int TILE = 16 * 1024;  // one [128][64] bf16 SW128 tile
 constexpr int KS = 3, VS = 3;    // K / V ring depth
-constexpr int ATT_THREADS = 384;  // 0 TMA, 1-2 MMA (slot A / B), 3 idle, 4-7 softmax A, 8-11 softmax B
-constexpr int SMEM_ATT = 1024 + 4 * TILE /*Q_A,Q_B x 2 units*/ + KS * TILE + VS * TILE + 256;
+constexpr int ATT_THREADS = 640;  // 0 TMA, 1-2 MMA (slot A / B), 3 idle, 4-11 softmax A, 12-19 softmax B
+constexpr int XCH_BYTES = 2 * 3 * 2 * 128 * 4;  // row max / sum exchange [slot][tile parity | epi][half][row]
+constexpr int SMEM_ATT = 1024 + 4 * TILE /*Q_A,Q_B x 2 units*/ + KS * TILE + VS * TILE + XCH_BYTES + 256;
 constexpr uint32_t S_COL = 0, P_COL = 256, O_COL = 384;
 }  // namespace
 
@@ -201,7 +203,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint8_t* sQ = smem;               // [2 units][2 slots]: the next unit's Q lands during this one
   uint8_t* sK = sQ + 4 * TILE;      // [KS]
   uint8_t* sV = sK + KS * TILE;     // [VS]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VS * TILE);
+  float* xch = reinterpret_cast<float*>(sV + VS * TILE);  // [2 slots][3][2 halves][128 rows]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + VS * TILE + XCH_BYTES);
   uint64_t* q_full = bars;          // [2 units][2 slots]
   uint64_t* q_empty = bars + 4;     // [2 units][2 slots]
   uint64_t* k_full = bars + 8;      // [KS]
@@ -228,8 +231,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&p_full[i], 8);
       mbar_init(&o_done[i], 1);
     }
     for (int i = 0; i < KS; ++i) {
@@ -344,18 +347,23 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   } else if (warp == 3) {
     // idle: completes warpgroup 0
   } else {
-    // softmax warps: x = Q slot, quadrant = warp % 4 (TMEM lanes 32*quadrant ..)
-    const int x = (warp >= 8) ? 1 : 0;
+    // softmax warps: Q slot x, column half hh (keys 64*hh .. 64*hh+63 of each tile), TMEM lane
+    // quadrant = warp % 4. The two warps of a (slot, quadrant) own the same 32 rows and agree on
+    // the row max through smem + a 64-thread named barrier.
+    const int sw = (int)warp - 4;
+    const int x = sw >> 3, hh = (sw >> 2) & 1;
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
+    const int bar_id = 1 + x * 4 + quad;  // named barrier of the warp pair
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
-    const uint32_t s_addr = lane_base + S_COL + x * 128;
-    const uint32_t p_addr = lane_base + P_COL + x * 64;
+    const uint32_t s_addr = lane_base + S_COL + x * 128 + hh * 64;
+    const uint32_t p_addr = lane_base + P_COL + x * 64 + hh * 32;
     const uint32_t o_addr = lane_base + O_COL + x * 64;
     int ns = 0, npv = 0;  // S tiles consumed, P tiles produced (global counts)
     int tn = 0;
-    const bool tr = (quad == 0 && lane == 0);
+    const bool tr = (quad == 0 && lane == 0 && hh == 0);
     const int tbase = 2048 + 1024 * x;
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const AttnUnit w = unit_of(u, BH, heads, T);
       if (x == 1 && !w.has_b) continue;
@@ -367,14 +375,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         mbar_wait(&s_full[x], ns & 1);
         tc_fence_after();
         if (tr) ATT_TRACE(tbase, tn, 11);
-        auto release_s = [&]() {  // every load of S_x(j) has landed in registers
+        auto release_s = [&]() {  // every load of this half of S_x(j) has landed in registers
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_free[x]);
         };
         if (warp_active) {
-          const int kvalid = T - j * 128;  // keys >= kvalid are padding / the next image
-          const int nch = kvalid >= 128 ? 4 : (kvalid + 31) >> 5;  // chunks holding a valid key
+          const int kvalid = T - j * 128 - hh * 64;  // keys of this half >= kvalid are padding
+          const int nch = kvalid >= 64 ? 2 : (kvalid <= 0 ? 0 : (kvalid + 31) >> 5);
           auto mask = [&](int c, float (&v)[32]) {
             if (c * 32 + 32 > kvalid) {
 #pragma unroll
@@ -382,35 +390,22 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
                 if (c * 32 + i >= kvalid) v[i] = -INFINITY;
             }
           };
-          float va[32], vb[32];
-          // pass 1: exact row max of the tile (S stays in TMEM; two chunks in flight)
-          float mx;
-          {
-            tmem_ld32(s_addr, va);
-            if (nch > 1) tmem_ld32(s_addr + 32, vb);
-            tmem_ld_wait_dep(va);
-            if (nch > 1) tmem_ld_wait_dep(vb);
-            mask(0, va);
-            mx = chunk_max_log2(va, scale_log2);
-            if (nch > 1) {
-              mask(1, vb);
-              mx = fmaxf(mx, chunk_max_log2(vb, scale_log2));
-            }
-            if (nch > 2) {
-              tmem_ld32(s_addr + 64, va);
-              if (nch > 3) tmem_ld32(s_addr + 96, vb);
-              tmem_ld_wait_dep(va);
-              if (nch > 3) tmem_ld_wait_dep(vb);
-              mask(2, va);
-              mx = fmaxf(mx, chunk_max_log2(va, scale_log2));
-              if (nch > 3) {
-                mask(3, vb);
-                mx = fmaxf(mx, chunk_max_log2(vb, scale_log2));
-              }
-            }
+          // pass 1: row max over this half (one 32-column chunk in registers at a time)
+          float mx = -INFINITY;
+#pragma unroll 1
+          for (int c = 0; c < nch; ++c) {
+            float v[32];
+            tmem_ld32(s_addr + c * 32, v);
+            tmem_ld_wait_dep(v);
+            mask(c, v);
+            mx = fmaxf(mx, chunk_max_log2(v, scale_log2));
           }
+          float* xrow = xch + ((x * 3 + (ns & 1)) * 2) * 128;
+          xrow[hh * 128 + r] = mx;
+          pair_sync();
+          mx = fmaxf(mx, xrow[(hh ^ 1) * 128 + r]);
           // the exponent offset m_used only moves when a row max exceeds it by > 8 (p <= 256),
-          // so O is rescaled in TMEM about once per row
+          // so O is rescaled in TMEM about once per row; both halves take identical decisions
           const bool raise = mx > m_used + 8.f;
           const bool rescale = __any_sync(0xffffffffu, raise);
           float alpha = 1.f;
@@ -426,31 +421,26 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             tc_fence_after();
           }
           if (tr) ATT_TRACE(tbase, tn, 12);
-          // pass 2: p = 2^(s*scale - m_used) chunk by chunk, next chunk in flight
+          // pass 2: p = 2^(s*scale - m_used) for this half's two chunks
           uint64_t lt = 0;  // f32x2 partial row sums
-          tmem_ld32(s_addr, va);
-          tmem_ld_wait_dep(va);
-          if (nch == 1) release_s();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float(&cur)[32] = (c & 1) ? vb : va;
-            float(&nxt)[32] = (c & 1) ? va : vb;
-            if (c + 1 < nch) tmem_ld32(s_addr + (c + 1) * 32, nxt);
+          for (int c = 0; c < 2; ++c) {
             if (c < nch) {
-              mask(c, cur);
-              lt = fadd2(lt, emit_chunk<POLY>(cur, scale_log2, m_used, p_addr + c * 16, c * 32 + 32 <= kvalid));
+              float v[32];
+              tmem_ld32(s_addr + c * 32, v);
+              tmem_ld_wait_dep(v);
+              if (c + 1 >= nch) release_s();
+              mask(c, v);
+              lt = fadd2(lt, emit_chunk<POLY>(v, scale_log2, m_used, p_addr + c * 16, c * 32 + 32 <= kvalid));
             } else {
+              if (c == 0) release_s();
               uint32_t pk[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i) pk[i] = 0u;
               tmem_st16u(p_addr + c * 16, pk);
             }
-            if (c + 1 < nch) {
-              tmem_ld_wait_dep(nxt);
-              if (c + 2 == nch) release_s();
-            }
           }
-          if (rescale && j > 0) {  // O_x *= alpha in TMEM (warp-collective; alpha = 1 on unchanged rows)
+          if (rescale && j > 0 && hh == 0) {  // O_x *= alpha in TMEM, done once per row (half 0)
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
               float t[32];
@@ -471,20 +461,23 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (tr) ATT_TRACE(tbase, tn, 13);
-        if (lane == 0) mbar_arrive(&p_full[x]);  // P_x(j) in TMEM
+        if (lane == 0) mbar_arrive(&p_full[x]);  // this half of P_x(j) in TMEM
       }
-      // epilogue: O_x / l -> ctx rows
+      // epilogue: l = l_half0 + l_half1; each half writes 32 of the 64 output columns
       mbar_wait(&o_done[x], (npv - 1) & 1);
       tc_fence_after();
       if (warp_active) {
-        float t[32], t2[32];
-        tmem_ld32(o_addr, t);
-        tmem_ld32(o_addr + 32, t2);
+        float* xrow = xch + ((x * 3 + 2) * 2) * 128;  // own slot: the next tile's max exchange may start
+        xrow[hh * 128 + r] = l;
+        pair_sync();
+        const float lsum = l + xrow[(hh ^ 1) * 128 + r];
+        float t[32];
+        tmem_ld32(o_addr + hh * 32, t);
         tmem_ld_wait();
         const int qi = q0 + r;
         if (qi < T) {
-          const float inv = kTruncScale / l;
-          uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(w.b * T + qi) * D + w.h * 64);
+          const float inv = kTruncScale / lsum;
+          uint4* dst = reinterpret_cast<uint4*>(out + (int64_t)(w.b * T + qi) * D + w.h * 64 + hh * 32);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint4 a;
@@ -493,12 +486,6 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             a.z = pack_bf16(t[8 * c + 4] * inv, t[8 * c + 5] * inv);
             a.w = pack_bf16(t[8 * c + 6] * inv, t[8 * c + 7] * inv);
             dst[c] = a;
-            uint4 b2;
-            b2.x = pack_bf16(t2[8 * c + 0] * inv, t2[8 * c + 1] * inv);
-            b2.y = pack_bf16(t2[8 * c + 2] * inv, t2[8 * c + 3] * inv);
-            b2.z = pack_bf16(t2[8 * c + 4] * inv, t2[8 * c + 5] * inv);
-            b2.w = pack_bf16(t2[8 * c + 6] * inv, t2[8 * c + 7] * inv);
-            dst[4 + c] = b2;
           }
         }
       }
