@@ -159,6 +159,11 @@ int vpe_vit_create(const vpe_vit_config* cfg, const vpe_vit_weights* w, vpe_vit*
 int vpe_vit_destroy(vpe_vit* v);
 /* pixels: u8 [B,3,R,R] device; taps: 4 device pointers to bf16 [B,T,D] (ring slot labels) */
 int vpe_vit_forward(vpe_vit* v, const void* pixels_u8, void* const* taps, void* stream);
+/* Camera ingest fused into the patch embedding: frames_hwc_u8 is [batch, height,
+ * width, 3] u8 (any size): centre-cropped to a square, bilinearly resized to resolution
+ * (align_corners=False, no antialias), ImageNet-normalised, then the same forward. */
+int vpe_vit_forward_camera(vpe_vit* v, const void* frames_hwc_u8, int32_t height, int32_t width,
+                           void* const* taps, void* stream);
 /* debug: fp32 residual stream [B*T, D] after the last forward */
 int vpe_vit_residual(vpe_vit* v, const float** resid);
 
@@ -245,6 +250,9 @@ int vpe_det_forward(vpe_det* d, const void* final_tap, const vpe_det_outputs* ou
 int vpe_op_linear(const void* A, int32_t M, int32_t K, const void* W, int32_t N, int32_t Kw, const float* bias,
                   const float* scale, void* out, int32_t kind, int32_t act, int32_t bn, void* stream);
 /* bn > 0: one-CTA 128 x bn tiles; bn < 0: CTA-pair (cta_group::2) 256 x |bn| tiles */
+/* camera ingest alone: [B,H,W,3] u8 -> normalised bf16 patch rows [B*(R/14)^2, 640] (k = c*196+ky*14+kx) */
+int vpe_op_camera_im2col(const void* frames_hwc_u8, int32_t B, int32_t height, int32_t width, int32_t resolution,
+                         void* out_bf16, void* stream);
 /* 3x3 or 1x1 same-padding conv on NHWC bf16 x [B,H,W,Cp] with weights [N, ks*ks*Cp] -> out bf16 NHWC
  * [B,H,W,ldo]; out = act(conv + bias + add1 + add2); out_relu optional */
 int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32_t Cp, int32_t ks, const void* w,

@@ -67,8 +67,9 @@ def block(h: torch.Tensor, W: dict, i: int, heads: int, eps: float) -> torch.Ten
 
 
 def embed(frames_u8: torch.Tensor, W: dict) -> torch.Tensor:
-    """preprocess + patch conv + cls + interpolated pos -> [B, T, D] fp32."""
-    x = preprocess(frames_u8)
+    """preprocess + patch conv + cls + interpolated pos -> [B, T, D] fp32. A floating-point input
+    is taken as already normalised (camera ingest: oracle/camera.py camera_preprocess)."""
+    x = frames_u8 if frames_u8.is_floating_point() else preprocess(frames_u8)
     B, _, R, _ = x.shape
     e = F.conv2d(x, W["embeddings.patch_embeddings.projection.weight"],
                  W["embeddings.patch_embeddings.projection.bias"], stride=14)

@@ -125,6 +125,8 @@ _SIGS = {
     "vpe_vit_destroy": (i32, [vp]),
     "vpe_vit_forward": (i32, [vp, vp, C.POINTER(vp), vp]),
     "vpe_vit_residual": (i32, [vp, C.POINTER(vp)]),
+    "vpe_vit_forward_camera": (i32, [vp, vp, i32, i32, C.POINTER(vp), vp]),
+    "vpe_op_camera_im2col": (i32, [vp, i32, i32, i32, i32, vp, vp]),
     "vpe_dpt_create": (i32, [C.POINTER(DptConfigC), C.POINTER(DptWeightsC), C.POINTER(vp)]),
     "vpe_dpt_destroy": (i32, [vp]),
     "vpe_dpt_forward": (i32, [vp, C.POINTER(vp), vp, vp, vp]),

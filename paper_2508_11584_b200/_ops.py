@@ -58,3 +58,12 @@ def layernorm(x: torch.Tensor, w, b, eps=1e-6, w2=None, b2=None, stream=None):
     check(lib.vpe_op_layernorm(_p(x), M, D, _p(w), _p(b), eps, _p(out), _p(w2), _p(b2), _p(out2), _s(stream)),
           "vpe_op_layernorm")
     return out if out2 is None else (out, out2)
+
+
+def camera_im2col(frames_hwc: torch.Tensor, resolution: int, stream=None) -> torch.Tensor:
+    """u8 [B,H,W,3] -> normalised bf16 patch rows [B*(R/14)^2, 640] (crop, resize, normalise fused)."""
+    B, H, W, _ = frames_hwc.shape
+    n = B * (resolution // 14) ** 2
+    out = torch.empty(n, 640, device=frames_hwc.device, dtype=torch.bfloat16)
+    check(lib.vpe_op_camera_im2col(_p(frames_hwc), B, H, W, resolution, _p(out), _s(stream)), "vpe_op_camera_im2col")
+    return out

@@ -108,6 +108,18 @@ class Backbone:
         check(lib.vpe_vit_forward(self._h, C.c_void_p(pixels_u8.data_ptr()), ptrs, C.c_void_p(stream)),
               "vpe_vit_forward")
 
+    def forward_camera(self, frames_hwc_u8: torch.Tensor, taps, stream: int | None = None) -> None:
+        """frames_hwc_u8: device u8 [B, H, W, 3] camera frames (any H, W): centre crop, bilinear
+        resize to R, normalisation and patch embedding in one kernel (vpe_vit_forward_camera)."""
+        if frames_hwc_u8.dim() != 4 or frames_hwc_u8.shape[-1] != 3 or frames_hwc_u8.dtype != torch.uint8:
+            raise ValueError(f"expected u8 [B,H,W,3], got {tuple(frames_hwc_u8.shape)} {frames_hwc_u8.dtype}")
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        ptrs = (C.c_void_p * 4)(*[t if isinstance(t, int) else t.data_ptr() for t in taps])
+        H, Wd = frames_hwc_u8.shape[1], frames_hwc_u8.shape[2]
+        check(lib.vpe_vit_forward_camera(self._h, C.c_void_p(frames_hwc_u8.data_ptr()), H, Wd, ptrs,
+                                         C.c_void_p(stream)), "vpe_vit_forward_camera")
+
     def residual(self) -> torch.Tensor:
         p = C.c_void_p()
         check(lib.vpe_vit_residual(self._h, C.byref(p)))

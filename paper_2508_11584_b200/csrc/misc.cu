@@ -49,6 +49,60 @@ int launch_patch_im2col(const uint8_t* px, __nv_bfloat16* A, int B, int R, int K
 }
 
 // ---------------------------------------------------------------------------------------------
+// Camera ingest fused into the patch embedding: u8 HWC camera frames
+// [B, Hc, Wc, 3] -> centre crop to the largest square -> bilinear resize to R x R (half-pixel
+// centres, align_corners=False, no antialias: torch F.interpolate) -> ImageNet normalisation ->
+// bf16 im2col rows, in one pass. Oracle: oracle/camera.py camera_preprocess.
+__global__ void camera_im2col_kernel(const uint8_t* __restrict__ hwc, int Hc, int Wc, __nv_bfloat16* __restrict__ A,
+                                     int B, int R, int KP, float* __restrict__ resid,
+                                     const float* __restrict__ cls_pos0, int D) {
+  const int h = R / 14, np = h * h;
+  const int blk = blockIdx.x;
+  if (blk >= B * np) {
+    const int b = blk - B * np;
+    float* dst = resid + (int64_t)b * (np + 1) * D;
+    for (int i = threadIdx.x; i < D; i += blockDim.x) dst[i] = cls_pos0[i];
+    return;
+  }
+  const int b = blk / np, p = blk - b * np;
+  const int py = p / h, pxx = p - py * h;
+  const int S = Hc < Wc ? Hc : Wc;
+  const int oy = (Hc - S) / 2, ox = (Wc - S) / 2;
+  const float scale = (float)S / (float)R;
+  const float mean[3] = {0.485f, 0.456f, 0.406f};
+  const float stdv[3] = {0.229f, 0.224f, 0.225f};
+  const uint8_t* img = hwc + (int64_t)b * Hc * Wc * 3;
+  __nv_bfloat16* row = A + (int64_t)blk * KP;
+  for (int k = threadIdx.x; k < KP; k += blockDim.x) {
+    float v = 0.f;
+    if (k < 588) {
+      const int c = k / 196, r = k - c * 196, ky = r / 14, kx = r - ky * 14;
+      const int y = py * 14 + ky, x = pxx * 14 + kx;
+      float sy = (y + 0.5f) * scale - 0.5f, sx = (x + 0.5f) * scale - 0.5f;
+      sy = sy < 0.f ? 0.f : sy;
+      sx = sx < 0.f ? 0.f : sx;
+      const int y0 = (int)sy, x0 = (int)sx;
+      const int y1 = y0 + (y0 < S - 1), x1 = x0 + (x0 < S - 1);
+      const float ly = sy - y0, lx = sx - x0, hy = 1.f - ly, hx = 1.f - lx;
+      const uint8_t* r0 = img + ((int64_t)(oy + y0) * Wc + ox) * 3 + c;
+      const uint8_t* r1 = img + ((int64_t)(oy + y1) * Wc + ox) * 3 + c;
+      const float u = hy * (hx * (float)__ldg(r0 + x0 * 3) + lx * (float)__ldg(r0 + x1 * 3)) +
+                      ly * (hx * (float)__ldg(r1 + x0 * 3) + lx * (float)__ldg(r1 + x1 * 3));
+      v = (u / 255.0f - mean[c]) / stdv[c];
+    }
+    row[k] = __float2bfloat16_rn(v);
+  }
+}
+
+int launch_camera_im2col(const uint8_t* hwc, int Hc, int Wc, __nv_bfloat16* A, int B, int R, int KP, float* resid,
+                         const float* cls_pos0, int D, cudaStream_t s) {
+  if (Hc < 1 || Wc < 1 || R % 14) return VPE_E_SHAPE;
+  const int np = (R / 14) * (R / 14);
+  camera_im2col_kernel<<<B * np + B, 128, 0, s>>>(hwc, Hc, Wc, A, B, R, KP, resid, cls_pos0, D);
+  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------------------------
 // LayerNorm over D (multiple of 128) for fp32 rows -> bf16; optional second affine (tap LN).
 // Two-pass mean/variance in registers (matches torch's reduction numerics closely).
 template <int NV>

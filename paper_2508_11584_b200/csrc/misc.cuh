@@ -6,6 +6,8 @@
 namespace vpe {
 int launch_patch_im2col(const uint8_t* px, __nv_bfloat16* A, int B, int R, int KP, float* resid,
                         const float* cls_pos0, int D, cudaStream_t s);
+int launch_camera_im2col(const uint8_t* hwc, int Hc, int Wc, __nv_bfloat16* A, int B, int R, int KP, float* resid,
+                         const float* cls_pos0, int D, cudaStream_t s);
 int launch_layernorm(const float* x, int M, int D, const float* w, const float* b, float eps, __nv_bfloat16* out,
                      const float* w2, const float* b2, __nv_bfloat16* out2, cudaStream_t s);
 int launch_bilinear_ac(const __nv_bfloat16* in, int B, int Hi, int Wi, int cp, __nv_bfloat16* out, int Ho, int Wo,

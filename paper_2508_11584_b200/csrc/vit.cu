@@ -142,15 +142,11 @@ extern "C" int vpe_vit_residual(vpe_vit* v, const float** resid) {
   return VPE_OK;
 }
 
-extern "C" int vpe_vit_forward(vpe_vit* v, const void* pixels_u8, void* const* taps, void* stream) {
-  if (!v || !pixels_u8 || !taps) return VPE_E_VALUE;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+// Shared tail of both entry points: patch GEMM, the L blocks, final LN into taps[3].
+static int vit_blocks(vpe_vit* v, void* const* taps, cudaStream_t s) {
   const vpe_vit_config& c = v->cfg;
   const vpe_vit_weights& w = v->w;
   const int D = c.dim, M = v->M;
-  VPE_TRY(launch_patch_im2col(static_cast<const uint8_t*>(pixels_u8), v->im2col, c.batch, c.resolution, KPATCH,
-                              v->resid, w.cls_pos0, D, s));
-  count_launches(1);
   VPE_TRY(launch_gemm(v->patch, s));
   count_launches(1);
   int tap = 0;
@@ -170,6 +166,39 @@ extern "C" int vpe_vit_forward(vpe_vit* v, const void* pixels_u8, void* const* t
   }
   VPE_TRY(launch_layernorm(v->resid, M, D, w.norm_w, w.norm_b, c.ln_eps, static_cast<__nv_bfloat16*>(taps[3]),
                            nullptr, nullptr, nullptr, s));
+  count_launches(1);
+  return VPE_OK;
+}
+
+extern "C" int vpe_vit_forward(vpe_vit* v, const void* pixels_u8, void* const* taps, void* stream) {
+  if (!v || !pixels_u8 || !taps) return VPE_E_VALUE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const vpe_vit_config& c = v->cfg;
+  VPE_TRY(launch_patch_im2col(static_cast<const uint8_t*>(pixels_u8), v->im2col, c.batch, c.resolution, KPATCH,
+                              v->resid, v->w.cls_pos0, c.dim, s));
+  count_launches(1);
+  return vit_blocks(v, taps, s);
+}
+
+extern "C" int vpe_vit_forward_camera(vpe_vit* v, const void* frames_hwc_u8, int32_t height, int32_t width,
+                                      void* const* taps, void* stream) {
+  if (!v || !frames_hwc_u8 || !taps) return VPE_E_VALUE;
+  if (height < 1 || width < 1) return VPE_E_SHAPE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const vpe_vit_config& c = v->cfg;
+  VPE_TRY(launch_camera_im2col(static_cast<const uint8_t*>(frames_hwc_u8), height, width, v->im2col, c.batch,
+                               c.resolution, KPATCH, v->resid, v->w.cls_pos0, c.dim, s));
+  count_launches(1);
+  return vit_blocks(v, taps, s);
+}
+
+extern "C" int vpe_op_camera_im2col(const void* frames_hwc_u8, int32_t B, int32_t height, int32_t width,
+                                    int32_t resolution, void* out_bf16, void* stream) {
+  if (!frames_hwc_u8 || !out_bf16 || B < 1 || resolution % 14) return VPE_E_VALUE;
+  // im2col rows only: a scratch cls/residual target is not needed (D = 0 writes nothing)
+  VPE_TRY(launch_camera_im2col(static_cast<const uint8_t*>(frames_hwc_u8), height, width,
+                               static_cast<__nv_bfloat16*>(out_bf16), B, resolution, KPATCH, nullptr, nullptr, 0,
+                               static_cast<cudaStream_t>(stream)));
   count_launches(1);
   return VPE_OK;
 }

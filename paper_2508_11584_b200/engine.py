@@ -91,7 +91,8 @@ class VPEngine:
     def __init__(self, model: str = "vits14", resolution: int = 448, batch: int = 1,
                  heads=("depth", "seg", "det"), capacity: int | None = None, rates: dict | None = None,
                  device: int = 0, weights: dict | None = None, graphs: bool = True, seed: int = 0,
-                 namespace: str | None = None, max_latency_records: int = 4096):
+                 namespace: str | None = None, max_latency_records: int = 4096,
+                 camera: tuple[int, int] | None = None):
         torch.cuda.set_device(device)
         self.device = torch.device(f"cuda:{device}")
         self.cfg = model_config(model)
@@ -129,7 +130,13 @@ class VPEngine:
             else:
                 self.gates[n] = make_gate(rate_hz=r, now_ns=now)
         R, B, dev = resolution, batch, self.device
-        self.pixels = torch.zeros(B, 3, R, R, dtype=torch.uint8, device=dev)
+        # camera=(H, W): frames arrive as u8 HWC camera images; crop/resize/normalise run fused
+        # into the patch embedding (vpe_vit_forward_camera) instead of expecting [B,3,R,R]
+        self.camera = tuple(camera) if camera else None
+        if self.camera:
+            self.pixels = torch.zeros(B, self.camera[0], self.camera[1], 3, dtype=torch.uint8, device=dev)
+        else:
+            self.pixels = torch.zeros(B, 3, R, R, dtype=torch.uint8, device=dev)
         self.out = {}
         if "depth" in self.heads:
             self.out["depth"] = {"depth": torch.zeros(B, R, R, device=dev), "depth_pre": torch.zeros(B, R, R, device=dev)}
@@ -169,7 +176,10 @@ class VPEngine:
         return [v[l] for l in self.labels]
 
     def _backbone_into(self, slot):
-        self.backbone.forward(self.pixels, self._taps(slot), stream=self.s_prod.handle)
+        if self.camera:
+            self.backbone.forward_camera(self.pixels, self._taps(slot), stream=self.s_prod.handle)
+        else:
+            self.backbone.forward(self.pixels, self._taps(slot), stream=self.s_prod.handle)
 
     def _head_on(self, name, slot):
         taps = self._taps(slot)

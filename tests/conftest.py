@@ -27,3 +27,10 @@ def device():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda:0")
+
+
+@pytest.fixture(scope="session")
+def ops():
+    """The libvpe single-op entry points (loads libvpe.so; fails loudly when it is missing)."""
+    from paper_2508_11584_b200 import _ops
+    return _ops
