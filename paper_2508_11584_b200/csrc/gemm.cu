@@ -628,28 +628,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 // ------------------------------------------------------------------------------------------
 // RT = output rows of 128 pixels per tile (W >= 128 only): RT accumulators of 128 x BN share one
 // (RT+2)-row halo, so the A traffic per output row drops from 3 to (RT+2)/RT halo rows.
-template <int BN, int KC, int RT>
+// WRES: every weight tile of the conv (parts x 9 taps x channel groups, <= 72 KB) is loaded
+// into shared memory once per CTA and stays resident for all of the CTA's tiles, so only the A
+// halo streams and the MMA issuer waits once per tile instead of once per tap (the DPT 3x3
+// convs: 64->64 RCUs 72 KB, head convs 36 / 18 KB).
+constexpr int WRES_BYTES = 72 * 1024;
+
+template <int BN, int KC, int RT, bool WRES = false>
 struct HaloCfg {
   static constexpr int GCH = 8 * KC;                 // channels per group
   static constexpr int A_MAX = KC * 130 * (RT + 2) * 16;  // largest halo stage (P=130)
   static constexpr int A_STAGES = 2;
   static constexpr int B_BYTES = BN * GCH * 2;       // one tap's weight tile
   static constexpr int B_STAGES = BN >= 128 ? 4 : 8;
+  static constexpr int B_REGION = WRES ? WRES_BYTES : B_STAGES * B_BYTES;
   static constexpr int TMEM_COLS = GemmCfg<BN * RT, 64>::TMEM_COLS;
   static constexpr int B_SWZ = GCH == 64 ? 2 : 4;
   static constexpr int B_SBO = 8 * GCH * 2;
-  static constexpr size_t SMEM = 1024 + (size_t)A_STAGES * A_MAX + (size_t)B_STAGES * B_BYTES + 256;
+  static constexpr size_t SMEM = 1024 + (size_t)A_STAGES * A_MAX + (size_t)B_REGION + 256;
 };
 
-template <int BN, int KC, int RT>
+template <int BN, int KC, int RT, bool WRES = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                      const GemmParams p) {
-  using C = HaloCfg<BN, KC, RT>;
+  using C = HaloCfg<BN, KC, RT, WRES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem;  // 1024-aligned for the swizzled weight tiles
-  uint8_t* sA = sB + C::B_STAGES * C::B_BYTES;
+  uint8_t* sA = sB + C::B_REGION;
   uint64_t* a_full = reinterpret_cast<uint64_t*>(sA + C::A_STAGES * C::A_MAX);
   uint64_t* a_empty = a_full + C::A_STAGES;
   uint64_t* b_full = a_empty + C::A_STAGES;
@@ -691,6 +698,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       int ia = 0, ib = 0;
+      if (WRES) {  // all weight tiles once (single N tile: the planner guarantees n_tiles == 1)
+        mbar_expect_tx(&b_full[0], groups * nb * C::B_BYTES);
+        for (int g = 0; g < groups; ++g)
+          for (int j = 0; j < nb; ++j) {
+            const int part = j / 9, tap = j - part * 9;
+            tma_load_2d(sB + (g * nb + j) * C::B_BYTES, &tb, &b_full[0], (part * 9 + tap) * p.kcp + g * C::GCH, 0);
+          }
+      }
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
         const int img = mt / p.tiles_per_img, rr = mt - img * p.tiles_per_img;
@@ -700,6 +715,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&a_empty[sa], ((ia / C::A_STAGES) & 1) ^ 1);
           mbar_expect_tx(&a_full[sa], a_bytes);
           tma_load_5d(sA + sa * C::A_MAX, &ta, &a_full[sa], 0, x0 - 1, y0 - 1, g * KC, img);
+          if (WRES) continue;
           for (int j = 0; j < nb; ++j, ++ib) {
             const int sb = ib % C::B_STAGES;
             mbar_wait(&b_empty[sb], ((ib / C::B_STAGES) & 1) ^ 1);
@@ -714,6 +730,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(128, BN);
       int ia = 0, ib = 0, i = 0;
+      if (WRES) {
+        mbar_wait(&b_full[0], 0);
+        tc_fence_after();
+      }
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
         const int acc = i & 1;
         mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
@@ -727,11 +747,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint32_t a0 = smem_u32(sA + sa * C::A_MAX);
           for (int j = 0; j < nb; ++j, ++ib) {
             const int sb = ib % C::B_STAGES;
-            mbar_wait(&b_full[sb], (ib / C::B_STAGES) & 1);
-            tc_fence_after();
+            if (!WRES) {
+              mbar_wait(&b_full[sb], (ib / C::B_STAGES) & 1);
+              tc_fence_after();
+            }
             const int tap = j % 9;
             const int dy = tap / 3, dx = tap - (tap / 3) * 3;
-            const uint32_t b0 = smem_u32(sB + sb * C::B_BYTES);
+            const uint32_t b0 = smem_u32(sB + (WRES ? (g * nb + j) : sb) * C::B_BYTES);
 #pragma unroll
             for (int rt = 0; rt < RT; ++rt) {
               const uint32_t at = a0 + (uint32_t)(((rt + dy) * P + dx) * 16);
@@ -743,7 +765,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               }
             }
             first = false;
-            umma_commit(&b_empty[sb]);
+            if (!WRES) umma_commit(&b_empty[sb]);
           }
           umma_commit(&a_empty[sa]);
         }
@@ -1086,23 +1108,27 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   g->bk = gch;
   g->halo_kc = kc;
   g->halo_rt = rt;
-#define VPE_HS(BN_, KC_, RT_) \
-  if (bn == BN_ && kc == KC_ && rt == RT_) g->smem = HaloCfg<BN_, KC_, RT_>::SMEM;
+  // weights resident in smem when the whole conv fits (single N tile)
+  g->halo_wres = (g->p.n_tiles == 1 && (size_t)parts * 9 * Cp * bn * 2 <= (size_t)WRES_BYTES &&
+                  !getenv("VPE_NO_WRES"));
+#define VPE_HS(BN_, KC_, RT_)                                                        \
+  if (bn == BN_ && kc == KC_ && rt == RT_)                                           \
+    g->smem = g->halo_wres ? HaloCfg<BN_, KC_, RT_, true>::SMEM : HaloCfg<BN_, KC_, RT_>::SMEM;
   VPE_HS(32, 4, 1) VPE_HS(64, 4, 1) VPE_HS(128, 4, 1) VPE_HS(32, 8, 1) VPE_HS(64, 8, 1) VPE_HS(128, 8, 1)
   VPE_HS(32, 4, 4) VPE_HS(32, 8, 2) VPE_HS(64, 8, 2)
 #undef VPE_HS
   return VPE_OK;
 }
 
-template <int BN, int KC, int RT>
+template <int BN, int KC, int RT, bool WRES = false>
 static int launch_halo_t(const GemmPlan& g, cudaStream_t s) {
-  auto k = conv_halo_kernel<BN, KC, RT>;
+  auto k = conv_halo_kernel<BN, KC, RT, WRES>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg<BN, KC, RT>::SMEM);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg<BN, KC, RT, WRES>::SMEM);
     attr_set = true;
   }
-  k<<<g.grid, GEMM_THREADS, HaloCfg<BN, KC, RT>::SMEM, s>>>(g.ta, g.tb, g.p);
+  k<<<g.grid, GEMM_THREADS, HaloCfg<BN, KC, RT, WRES>::SMEM, s>>>(g.ta, g.tb, g.p);
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
 }
 
@@ -1150,8 +1176,9 @@ int launch_gemm(const GemmPlan& g, cudaStream_t s) {
     return VPE_E_SHAPE;
   }
   if (g.halo_kc) {
-#define VPE_LH(BN_, KC_, RT_) \
-  if (g.bn == BN_ && g.halo_kc == KC_ && g.halo_rt == RT_) return launch_halo_t<BN_, KC_, RT_>(g, s);
+#define VPE_LH(BN_, KC_, RT_)                                                         \
+  if (g.bn == BN_ && g.halo_kc == KC_ && g.halo_rt == RT_)                            \
+    return g.halo_wres ? launch_halo_t<BN_, KC_, RT_, true>(g, s) : launch_halo_t<BN_, KC_, RT_>(g, s);
     VPE_LH(32, 4, 1) VPE_LH(64, 4, 1) VPE_LH(128, 4, 1) VPE_LH(32, 8, 1) VPE_LH(64, 8, 1) VPE_LH(128, 8, 1)
     VPE_LH(32, 4, 4) VPE_LH(32, 8, 2) VPE_LH(64, 8, 2)
 #undef VPE_LH

@@ -71,6 +71,7 @@ struct GemmPlan {
   int bn = 0, bk = 0;
   int halo_kc = 0;  // > 0: conv_halo_kernel<bn, halo_kc, halo_rt>
   int halo_rt = 1;
+  int halo_wres = 0;  // 1: conv_halo_kernel<.., WRES> (all weight tiles resident in smem)
   int pair = 0;     // 1: gemm_pair_kernel<bn> (cta_group::2, 256-row tiles)
   size_t smem = 0;
 };
