@@ -165,8 +165,8 @@ VPE_DEV void epilogue_direct(const EpiParams& ep, int64_t gpix, int col0, float 
       break;
     }
     case EPI_PATCH: {
-      const int64_t img = gpix / ep.rows_per_img;
-      const int64_t p = gpix - img * ep.rows_per_img;
+      const int img = (int)gpix / ep.rows_per_img;  // 32-bit: rows < 2^31
+      const int64_t p = gpix - (int64_t)img * ep.rows_per_img;
       float* r = ep.resid + (gpix + img + 1) * ep.ldr + col0;
       add_vec32(v, ep.pos + (p + 1) * (int64_t)N, col0, N, full);
       if (full) {
@@ -198,8 +198,8 @@ VPE_DEV void epilogue_direct(const EpiParams& ep, int64_t gpix, int col0, float 
     case EPI_CONVT: {
       // gpix indexes the input grid (img, y, x); each group of ct_cout columns is one sub-pixel.
       const int HW = ep.ct_H * ep.ct_W;
-      const int64_t img = gpix / HW;
-      const int rem = (int)(gpix - img * HW);
+      const int img = (int)gpix / HW;  // 32-bit: pixels < 2^31
+      const int rem = (int)gpix - img * HW;
       const int y = rem / ep.ct_W, x = rem - (rem / ep.ct_W) * ep.ct_W;
       // ct_cout is a multiple of 32, so a 32-column chunk is 32 contiguous channels of one
       // output sub-pixel: one 64-byte vector store

@@ -181,16 +181,18 @@ template <int NV>
 __global__ void __launch_bounds__(256) bilinear_ac_kernel(const __nv_bfloat16* __restrict__ in, int B, int Hi,
                                                           int Wi, int cp, __nv_bfloat16* __restrict__ out, int Ho,
                                                           int Wo, int C) {
+  // 32-bit index math (64-bit div/mod is a long software sequence; B*Ho*Wo*groups < 2^31 is
+  // checked by the launcher)
   const int groups = C / (8 * NV);
-  const int64_t total = (int64_t)B * Ho * Wo * groups;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int total = B * Ho * Wo * groups;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
-  const int g = (int)(t % groups);
-  int64_t pix = t / groups;
-  const int ox = (int)(pix % Wo);
+  const int g = groups == 1 ? 0 : t % groups;
+  int pix = groups == 1 ? t : t / groups;
+  const int ox = pix % Wo;
   pix /= Wo;
-  const int oy = (int)(pix % Ho);
-  const int b = (int)(pix / Ho);
+  const int oy = pix % Ho;
+  const int b = pix / Ho;
   const float sh = Ho > 1 ? (float)(Hi - 1) / (float)(Ho - 1) : 0.f;
   const float sw = Wo > 1 ? (float)(Wi - 1) / (float)(Wo - 1) : 0.f;
   const float fy = sh * oy, fx = sw * ox;
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(256) bilinear_ac_kernel(const __nv_bfloat16* _
 int launch_bilinear_ac(const __nv_bfloat16* in, int B, int Hi, int Wi, int cp, __nv_bfloat16* out, int Ho, int Wo,
                        int C, cudaStream_t s) {
   if (C % 8 || cp % 8) return VPE_E_SHAPE;
+  if ((int64_t)B * Ho * Wo * (C / 8) >= (int64_t)1 << 31) return VPE_E_SHAPE;
   const int nv = (C % 32 == 0) ? 4 : 1;
   const int64_t total = (int64_t)B * Ho * Wo * (C / (8 * nv));
   const unsigned blocks = (unsigned)((total + 255) / 256);
@@ -250,17 +253,17 @@ int launch_bilinear_ac(const __nv_bfloat16* in, int B, int Hi, int Wi, int cp, _
 __global__ void im2col_s2_kernel(const __nv_bfloat16* __restrict__ x, int B, int H, int W, int C,
                                  __nv_bfloat16* __restrict__ out, int Ho, int Wo) {
   const int cv = C / 8;
-  const int64_t total = (int64_t)B * Ho * Wo * 9 * cv;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int total = B * Ho * Wo * 9 * cv;  // < 2^31 (checked by the launcher): 32-bit div/mod
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= total) return;
-  const int c8 = (int)(t % cv);
-  int64_t r = t / cv;
-  const int tap = (int)(r % 9);
+  const int c8 = t % cv;
+  int r = t / cv;
+  const int tap = r % 9;
   r /= 9;
-  const int ox = (int)(r % Wo);
+  const int ox = r % Wo;
   r /= Wo;
-  const int oy = (int)(r % Ho);
-  const int b = (int)(r / Ho);
+  const int oy = r % Ho;
+  const int b = r / Ho;
   const int iy = 2 * oy - 1 + tap / 3, ix = 2 * ox - 1 + tap % 3;
   uint4 v = make_uint4(0, 0, 0, 0);
   if (iy >= 0 && iy < H && ix >= 0 && ix < W)
@@ -272,6 +275,7 @@ int launch_im2col_s2(const __nv_bfloat16* x, int B, int H, int W, int C, __nv_bf
   if (C % 8) return VPE_E_SHAPE;
   const int Ho = (H + 1) / 2, Wo = (W + 1) / 2;
   const int64_t total = (int64_t)B * Ho * Wo * 9 * (C / 8);
+  if (total >= ((int64_t)1 << 31)) return VPE_E_SHAPE;
   im2col_s2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(x, B, H, W, C, out, Ho, Wo);
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
 }
