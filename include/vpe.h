@@ -97,6 +97,13 @@ typedef struct {
 int vpe_ring_create(const vpe_tensor_spec* specs, int32_t nspecs, int32_t capacity, int32_t mode, int32_t device,
                     vpe_ring** out);
 int vpe_ring_destroy(vpe_ring* r);
+/* Cross-process rings (channels.py:537-594 create_channel / open_channel across processes):
+ * the control block goes to POSIX shm "/vpe.<name>-c", the HBM arena and the ready/done events
+ * are exported through CUDA IPC (handles in "/vpe.<name>-x"); a VPE_HOST_PLAIN ring keeps its
+ * data in "/vpe.<name>-d". The creator unlinks the segments on destroy. */
+int vpe_ring_create_shared(const vpe_tensor_spec* specs, int32_t nspecs, int32_t capacity, int32_t mode,
+                           int32_t device, const char* name, vpe_ring** out);
+int vpe_ring_attach(const char* name, vpe_ring** out);
 int vpe_ring_header(vpe_ring* r, void** base, size_t* size);
 int vpe_ring_data(vpe_ring* r, void** base, size_t* size);
 int vpe_ring_slot_ptr(vpe_ring* r, int32_t slot, int32_t label, void** ptr);

@@ -103,6 +103,8 @@ _SIGS = {
     # ring
     "vpe_ring_create": (i32, [C.POINTER(TensorSpecC), i32, i32, i32, i32, C.POINTER(vp)]),
     "vpe_ring_destroy": (i32, [vp]),
+    "vpe_ring_create_shared": (i32, [C.POINTER(TensorSpecC), i32, i32, i32, i32, C.c_char_p, C.POINTER(vp)]),
+    "vpe_ring_attach": (i32, [C.c_char_p, C.POINTER(vp)]),
     "vpe_ring_header": (i32, [vp, C.POINTER(vp), C.POINTER(C.c_size_t)]),
     "vpe_ring_data": (i32, [vp, C.POINTER(vp), C.POINTER(C.c_size_t)]),
     "vpe_ring_slot_ptr": (i32, [vp, i32, i32, C.POINTER(vp)]),

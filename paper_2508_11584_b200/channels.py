@@ -393,8 +393,9 @@ class Channel:
             self._raw = None
             lib.vpe_ring_destroy(self._ring)
             self._ring = None
-            ar.forget_allocation(self.handle.data.os_name)
-            ar.forget_allocation(self.handle.header.os_name)
+            if not getattr(self, "_attached", False):
+                ar.forget_allocation(self.handle.data.os_name)
+                ar.forget_allocation(self.handle.header.os_name)
 
     def unlink(self) -> None:
         self.close()
@@ -406,11 +407,17 @@ def header_region_bytes(capacity: int) -> int:
     return max(4096, (need + 4095) // 4096 * 4096)
 
 
+def _shared_name(handle: ChannelHandle) -> bytes:
+    return f"{handle.namespace}.{handle.name}".encode()
+
+
 def create_channel(name: str, mode: ChannelMode, capacity: int, slot_group: Sequence[ar.TensorSpec],
                    namespace: str, expected_consumers: int | None = None, device: int = 0,
-                   stream: int | None = None) -> tuple[Channel, ChannelHandle]:
+                   stream: int | None = None, shared: bool = False) -> tuple[Channel, ChannelHandle]:
     """Create the control block and the slot arena (HBM for device >= 0); all slots FREE.
-    Validation and warnings follow channels.py:537-576."""
+    Validation and warnings follow channels.py:537-576. ``shared=True`` puts the control block in
+    POSIX shared memory and exports the HBM arena and its events through CUDA IPC, so other
+    processes can ``open_channel(handle)`` (the reference's cross-process channel)."""
     if capacity < 2:
         raise ConfigError(f"channel capacity must be >= 2, got {capacity}")
     specs = tuple(slot_group)
@@ -439,11 +446,34 @@ def create_channel(name: str, mode: ChannelMode, capacity: int, slot_group: Sequ
         raise
     if device >= 0:
         torch.cuda.set_device(device)
-    rc = lib.vpe_ring_create(arr, len(specs), capacity, mode.value, device, C.byref(ring))
+    handle = ChannelHandle(name=name, namespace=namespace, mode=mode, capacity=capacity, specs=specs,
+                           header=hdr_h, data=data_h)
+    if shared:
+        rc = lib.vpe_ring_create_shared(arr, len(specs), capacity, mode.value, device, _shared_name(handle),
+                                        C.byref(ring))
+    else:
+        rc = lib.vpe_ring_create(arr, len(specs), capacity, mode.value, device, C.byref(ring))
     if rc:
         ar.forget_allocation(data_h.os_name)
         ar.forget_allocation(hdr_h.os_name)
     check(rc, "create_channel")
-    handle = ChannelHandle(name=name, namespace=namespace, mode=mode, capacity=capacity, specs=specs,
-                           header=hdr_h, data=data_h)
     return Channel(handle, ring, stream=stream), handle
+
+
+def open_channel(handle: ChannelHandle, stream: int | None = None) -> Channel:
+    """Attach to a channel created with ``shared=True`` in another process (channels.py:579-594):
+    maps the shared control block, opens the HBM arena and the ready/done events through CUDA
+    IPC, and validates the header (magic, mode, capacity) against the handle."""
+    ring = C.c_void_p()
+    if handle.data.device >= 0:
+        torch.cuda.set_device(handle.data.device)
+    check(lib.vpe_ring_attach(_shared_name(handle), C.byref(ring)), "open_channel")
+    ch = Channel(handle, ring, stream=stream)
+    hdr = ch.header_bytes()
+    cap = int.from_bytes(hdr[8:12], "little")
+    if hdr[:6] != b"PECH1\x00" or hdr[6] != handle.mode.value or cap != handle.capacity:
+        ch._attached = True
+        ch.close()
+        raise ConfigError(f"channel {handle.name}: header does not match the handle")
+    ch._attached = True
+    return ch

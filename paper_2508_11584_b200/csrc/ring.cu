@@ -14,9 +14,15 @@
 // its stream wait on every consumer's last done event for that slot (WAR). So host-side lease
 // counting orders the host, events order the device.
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <atomic>
+#include <cerrno>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -69,7 +75,12 @@ struct vpe_ring {
   size_t data_bytes = 0;
   cudaEvent_t* ready = nullptr;       // [capacity]
   cudaEvent_t* done = nullptr;        // [capacity * MAX_CONSUMERS]
-  uint8_t* done_valid = nullptr;      // [capacity * MAX_CONSUMERS]
+  uint8_t* done_valid = nullptr;      // [capacity * MAX_CONSUMERS] (in the IPC segment when shared)
+  // cross-process sharing: 0 private, 1 creator of the shm segments, 2 attached
+  int role = 0;
+  char nm_hdr[192] = {0}, nm_ipc[192] = {0}, nm_dat[192] = {0};
+  uint8_t* ipc = nullptr;
+  size_t ipc_bytes = 0;
   int64_t* pending_evict = nullptr;   // [capacity], -1 none
   uint64_t last_id = 0, last_ts = 0;
   int cursor_slot[VPE_MAX_CONSUMERS];
@@ -159,6 +170,26 @@ int vpe_ring_destroy(vpe_ring* r) {
   if (r->done)
     for (int i = 0; i < r->capacity * VPE_MAX_CONSUMERS; ++i)
       if (r->done[i]) cudaEventDestroy(r->done[i]);
+  if (r->role) {  // shared ring: unmap (and, for the creator, unlink) the POSIX segments
+    if (r->data) {
+      if (r->device == VPE_HOST_PLAIN)
+        munmap(r->data, r->data_bytes);
+      else if (r->role == 2)
+        cudaIpcCloseMemHandle(r->data);
+      else
+        cudaFree(r->data);
+    }
+    if (r->hdr) munmap(r->hdr, r->hdr_bytes);
+    if (r->ipc) munmap(r->ipc, r->ipc_bytes);
+    if (r->role == 1) {
+      shm_unlink(r->nm_hdr);
+      shm_unlink(r->nm_ipc);
+      if (r->device == VPE_HOST_PLAIN) shm_unlink(r->nm_dat);
+    }
+    r->data = nullptr;
+    r->hdr = nullptr;
+    r->done_valid = nullptr;
+  }
   if (r->data) {
     if (r->device == VPE_HOST_PLAIN)
       free(r->data);
@@ -167,13 +198,13 @@ int vpe_ring_destroy(vpe_ring* r) {
     else
       cudaFree(r->data);
   }
-  free(r->hdr);
+  if (!r->role) free(r->hdr);
   delete[] r->specs;
   delete[] r->nbytes;
   delete[] r->offsets;
   delete[] r->ready;
   delete[] r->done;
-  delete[] r->done_valid;
+  if (!r->role) delete[] r->done_valid;
   delete[] r->pending_evict;
   delete r;
   return VPE_OK;
@@ -358,7 +389,7 @@ int vpe_ring_claim(vpe_ring* r, uint64_t frame_id, uint64_t capture_ts, void* st
   if (r->device != VPE_HOST_PLAIN)
     for (int c = 0; c < VPE_MAX_CONSUMERS; ++c) {
       const int k = s * VPE_MAX_CONSUMERS + c;
-      if (r->done_valid[k]) VPE_CUDA_TRY(cudaStreamWaitEvent(st, r->done[k], 0));
+      if (__atomic_load_n(&r->done_valid[k], __ATOMIC_ACQUIRE)) VPE_CUDA_TRY(cudaStreamWaitEvent(st, r->done[k], 0));
     }
   return VPE_OK;
 }
@@ -474,7 +505,7 @@ static int finish(vpe_ring* r, vpe_lease* lease, void* stream) {
   const int k = lease->slot * VPE_MAX_CONSUMERS + cidx;
   if (stream && r->device != VPE_HOST_PLAIN) {
     VPE_CUDA_TRY(cudaEventRecord(r->done[k], static_cast<cudaStream_t>(stream)));
-    r->done_valid[k] = 1;
+    __atomic_store_n(&r->done_valid[k], (uint8_t)1, __ATOMIC_RELEASE);
   }
   st64(r->cursor(cidx) + 8, lease->frame_id);  // channels.py:470
   add64(r->consumed(), 1);
@@ -515,7 +546,7 @@ int vpe_ring_release(vpe_ring* r, vpe_lease* lease, void* stream) {
     if (cidx >= 0) {
       const int k = lease->slot * VPE_MAX_CONSUMERS + cidx;
       VPE_CUDA_TRY(cudaEventRecord(r->done[k], static_cast<cudaStream_t>(stream)));
-      r->done_valid[k] = 1;
+      __atomic_store_n(&r->done_valid[k], (uint8_t)1, __ATOMIC_RELEASE);
     }
   }
   VPE_TRY(release_slot(r, lease->slot));
@@ -595,6 +626,256 @@ int vpe_ring_slot_state(vpe_ring* r, int32_t slot, uint32_t* state, uint64_t* fi
   if (!r || slot < 0 || slot >= r->capacity) return VPE_E_NOT_FOUND;
   *state = ld32(r->state(slot));
   *fid = ld64(r->fid(slot));
+  return VPE_OK;
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Cross-process rings (PAPER.md:95-121 runs every head in its own process).
+// The reference shares its arena and channel header through POSIX shared memory
+// (arena.py:285-344, channels.py:537-594). Here the PECH1 control block lives in a POSIX
+// segment "<name>-c" (state words keep the same acquire/release CAS protocol across processes),
+// the HBM slot arena is exported with cudaIpcGetMemHandle, and the ready / done events are
+// created cudaEventInterprocess and exported with cudaIpcGetEventHandle; all handles plus the
+// shared done-valid flags sit in "<name>-x". A plain-host ring keeps its data in "<name>-d".
+namespace {
+constexpr char IPC_MAGIC[8] = {'P', 'E', 'I', 'P', 'C', '1', 0, 0};
+struct IpcHead {
+  char magic[8];
+  int32_t device, capacity, nspecs, mode;
+  uint64_t data_bytes, hdr_bytes;
+  cudaIpcMemHandle_t mem;
+};
+size_t ipc_layout(int capacity, int nspecs, size_t* off_specs, size_t* off_ready, size_t* off_done,
+                  size_t* off_valid) {
+  size_t o = align_up(sizeof(IpcHead), 64);
+  *off_specs = o;
+  o += align_up(sizeof(vpe_tensor_spec) * (size_t)nspecs, 64);
+  *off_ready = o;
+  o += sizeof(cudaIpcEventHandle_t) * (size_t)capacity;
+  *off_done = o;
+  o += sizeof(cudaIpcEventHandle_t) * (size_t)capacity * VPE_MAX_CONSUMERS;
+  *off_valid = o;
+  o += (size_t)capacity * VPE_MAX_CONSUMERS;
+  return align_up(o, 4096);
+}
+int shm_map(const char* name, size_t bytes, bool create, void** base, size_t* mapped) {
+  const int fd = shm_open(name, create ? (O_CREAT | O_EXCL | O_RDWR) : O_RDWR, 0600);
+  if (fd < 0) return errno == EEXIST ? VPE_E_ALREADY_EXISTS : (errno == ENOENT ? VPE_E_NOT_FOUND : VPE_E_RESOURCE);
+  if (create) {
+    if (ftruncate(fd, (off_t)bytes) != 0) {
+      close(fd);
+      shm_unlink(name);
+      return VPE_E_RESOURCE;
+    }
+  } else {
+    struct stat st;
+    if (fstat(fd, &st) != 0 || (size_t)st.st_size < 64) {
+      close(fd);
+      return VPE_E_CORRUPT_HANDLE;
+    }
+    bytes = (size_t)st.st_size;
+  }
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) {
+    if (create) shm_unlink(name);
+    return VPE_E_RESOURCE;
+  }
+  *base = p;
+  *mapped = bytes;
+  return VPE_OK;
+}
+void shm_names(vpe_ring* r, const char* name) {
+  snprintf(r->nm_hdr, sizeof(r->nm_hdr), "/vpe.%s-c", name);
+  snprintf(r->nm_ipc, sizeof(r->nm_ipc), "/vpe.%s-x", name);
+  snprintf(r->nm_dat, sizeof(r->nm_dat), "/vpe.%s-d", name);
+}
+}  // namespace
+
+int vpe_ring_create_shared(const vpe_tensor_spec* specs, int32_t nspecs, int32_t capacity, int32_t mode,
+                           int32_t device, const char* name, vpe_ring** out) {
+  if (!out || !name || !name[0] || strlen(name) > 150 || strchr(name, '/')) return VPE_E_CONFIG;
+  if (device == VPE_HOST_PINNED) return VPE_E_CONFIG;  // pinned host memory is not exportable here
+  // build the layout and CUDA objects privately first, then move the control block into shm
+  vpe_ring* r = nullptr;
+  VPE_TRY(vpe_ring_create(specs, nspecs, capacity, mode, device, &r));
+  shm_names(r, name);
+  size_t o_specs, o_ready, o_done, o_valid;
+  const size_t ipc_bytes = ipc_layout(capacity, nspecs, &o_specs, &o_ready, &o_done, &o_valid);
+  void* hdr = nullptr;
+  void* ipc = nullptr;
+  size_t hdr_map = 0, ipc_map = 0;
+  int rc = shm_map(r->nm_hdr, r->hdr_bytes, true, &hdr, &hdr_map);
+  if (rc) {
+    vpe_ring_destroy(r);
+    return rc;
+  }
+  rc = shm_map(r->nm_ipc, ipc_bytes, true, &ipc, &ipc_map);
+  if (rc) {
+    munmap(hdr, hdr_map);
+    shm_unlink(r->nm_hdr);
+    vpe_ring_destroy(r);
+    return rc;
+  }
+  memcpy(hdr, r->hdr, r->hdr_bytes);
+  free(r->hdr);
+  r->hdr = static_cast<uint8_t*>(hdr);
+  r->ipc = static_cast<uint8_t*>(ipc);
+  r->ipc_bytes = ipc_map;
+  memset(r->ipc, 0, ipc_map);
+  delete[] r->done_valid;
+  r->done_valid = r->ipc + o_valid;
+  r->role = 1;
+  IpcHead* h = reinterpret_cast<IpcHead*>(r->ipc);
+  memcpy(h->magic, IPC_MAGIC, 8);
+  h->device = device;
+  h->capacity = capacity;
+  h->nspecs = nspecs;
+  h->mode = mode;
+  h->data_bytes = r->data_bytes;
+  h->hdr_bytes = r->hdr_bytes;
+  memcpy(r->ipc + o_specs, specs, sizeof(vpe_tensor_spec) * (size_t)nspecs);
+  if (device == VPE_HOST_PLAIN) {
+    void* dat = nullptr;
+    size_t dat_map = 0;
+    if ((rc = shm_map(r->nm_dat, r->data_bytes, true, &dat, &dat_map))) {
+      vpe_ring_destroy(r);
+      return rc;
+    }
+    memcpy(dat, r->data, r->data_bytes);
+    free(r->data);
+    r->data = static_cast<uint8_t*>(dat);
+    *out = r;
+    return VPE_OK;
+  }
+  // device ring: export the arena and interprocess events
+  if (cudaIpcGetMemHandle(&h->mem, r->data) != cudaSuccess) {
+    vpe_ring_destroy(r);
+    return VPE_E_CUDA;
+  }
+  auto remake = [&](cudaEvent_t* e, cudaIpcEventHandle_t* eh) -> bool {
+    cudaEventDestroy(*e);
+    *e = nullptr;
+    return cudaEventCreateWithFlags(e, cudaEventDisableTiming | cudaEventInterprocess) == cudaSuccess &&
+           cudaIpcGetEventHandle(eh, *e) == cudaSuccess;
+  };
+  auto* ready_h = reinterpret_cast<cudaIpcEventHandle_t*>(r->ipc + o_ready);
+  auto* done_h = reinterpret_cast<cudaIpcEventHandle_t*>(r->ipc + o_done);
+  for (int i = 0; i < capacity; ++i)
+    if (!remake(&r->ready[i], &ready_h[i])) {
+      vpe_ring_destroy(r);
+      return VPE_E_CUDA;
+    }
+  for (int i = 0; i < capacity * VPE_MAX_CONSUMERS; ++i)
+    if (!remake(&r->done[i], &done_h[i])) {
+      vpe_ring_destroy(r);
+      return VPE_E_CUDA;
+    }
+  *out = r;
+  return VPE_OK;
+}
+
+int vpe_ring_attach(const char* name, vpe_ring** out) {
+  if (!out || !name || !name[0] || strlen(name) > 150 || strchr(name, '/')) return VPE_E_CONFIG;
+  vpe_ring* r = new (std::nothrow) vpe_ring();
+  if (!r) return VPE_E_RESOURCE;
+  shm_names(r, name);
+  r->role = 2;
+  void* ipc = nullptr;
+  size_t ipc_map = 0;
+  int rc = shm_map(r->nm_ipc, 0, false, &ipc, &ipc_map);
+  if (rc) {
+    delete r;
+    return rc;
+  }
+  r->ipc = static_cast<uint8_t*>(ipc);
+  r->ipc_bytes = ipc_map;
+  const IpcHead* h = reinterpret_cast<const IpcHead*>(r->ipc);
+  if (memcmp(h->magic, IPC_MAGIC, 8) != 0 || h->capacity < 2 || h->nspecs < 1) {
+    vpe_ring_destroy(r);
+    return VPE_E_CORRUPT_HANDLE;
+  }
+  size_t o_specs, o_ready, o_done, o_valid;
+  if (ipc_layout(h->capacity, h->nspecs, &o_specs, &o_ready, &o_done, &o_valid) > ipc_map) {
+    vpe_ring_destroy(r);
+    return VPE_E_CORRUPT_HANDLE;
+  }
+  // rebuild the layout from the published specs (same code path as the creator)
+  vpe_ring* tmp = nullptr;
+  const int dev_for_layout = VPE_HOST_PLAIN;  // layout only: no allocation of CUDA objects
+  (void)dev_for_layout;
+  r->nspecs = h->nspecs;
+  r->capacity = h->capacity;
+  r->mode = h->mode;
+  r->device = h->device;
+  r->specs = new vpe_tensor_spec[r->nspecs];
+  memcpy(r->specs, r->ipc + o_specs, sizeof(vpe_tensor_spec) * (size_t)r->nspecs);
+  r->nbytes = new size_t[r->nspecs];
+  for (int i = 0; i < r->nspecs; ++i) {
+    size_t n = itemsize(r->specs[i].dtype);
+    for (int d = 0; d < r->specs[i].rank; ++d) n *= (size_t)r->specs[i].dims[d];
+    r->nbytes[i] = n;
+  }
+  r->offsets = new size_t[(size_t)r->nspecs * r->capacity];
+  size_t cur = 0;
+  for (int sl = 0; sl < r->capacity; ++sl)
+    for (int l = 0; l < r->nspecs; ++l) {
+      const size_t off = align_up(cur, ALIGN);
+      r->offsets[sl * r->nspecs + l] = off;
+      cur = off + r->nbytes[l];
+    }
+  (void)tmp;
+  r->data_bytes = h->data_bytes;
+  r->pending_evict = new int64_t[r->capacity];
+  for (int i = 0; i < r->capacity; ++i) r->pending_evict[i] = -1;
+  r->ready = new cudaEvent_t[r->capacity]();
+  r->done = new cudaEvent_t[(size_t)r->capacity * VPE_MAX_CONSUMERS]();
+  r->done_valid = r->ipc + o_valid;
+  void* hdr = nullptr;
+  size_t hdr_map = 0;
+  if ((rc = shm_map(r->nm_hdr, 0, false, &hdr, &hdr_map))) {
+    vpe_ring_destroy(r);
+    return rc;
+  }
+  r->hdr = static_cast<uint8_t*>(hdr);
+  r->hdr_bytes = hdr_map;
+  if (memcmp(r->hdr, "PECH1\0", 6) != 0 || r->hdr[6] != (uint8_t)r->mode) {
+    vpe_ring_destroy(r);
+    return VPE_E_CORRUPT_HANDLE;
+  }
+  if (r->device == VPE_HOST_PLAIN) {
+    void* dat = nullptr;
+    size_t dat_map = 0;
+    if ((rc = shm_map(r->nm_dat, 0, false, &dat, &dat_map))) {
+      vpe_ring_destroy(r);
+      return rc;
+    }
+    r->data = static_cast<uint8_t*>(dat);
+    *out = r;
+    return VPE_OK;
+  }
+  void* dptr = nullptr;
+  if (cudaSetDevice(r->device) != cudaSuccess ||
+      cudaIpcOpenMemHandle(&dptr, h->mem, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    vpe_ring_destroy(r);
+    return VPE_E_CUDA;
+  }
+  r->data = static_cast<uint8_t*>(dptr);
+  auto* ready_h = reinterpret_cast<cudaIpcEventHandle_t*>(r->ipc + o_ready);
+  auto* done_h = reinterpret_cast<cudaIpcEventHandle_t*>(r->ipc + o_done);
+  for (int i = 0; i < r->capacity; ++i)
+    if (cudaIpcOpenEventHandle(&r->ready[i], ready_h[i]) != cudaSuccess) {
+      vpe_ring_destroy(r);
+      return VPE_E_CUDA;
+    }
+  for (int i = 0; i < r->capacity * VPE_MAX_CONSUMERS; ++i)
+    if (cudaIpcOpenEventHandle(&r->done[i], done_h[i]) != cudaSuccess) {
+      vpe_ring_destroy(r);
+      return VPE_E_CUDA;
+    }
+  *out = r;
   return VPE_OK;
 }
 
