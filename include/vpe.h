@@ -265,6 +265,10 @@ int vpe_op_camera_im2col(const void* frames_hwc_u8, int32_t B, int32_t height, i
 int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32_t Cp, int32_t ks, const void* w,
                 int32_t N, const float* bias, const void* add1, const void* add2, void* out, void* out_relu,
                 int32_t ldo, int32_t act, void* stream);
+/* fused MLP block: resid[M,D] += ls2 * (GELU(X W1^T + b1) W2^T + b2); X bf16 [M,D], W1 bf16 [hidden,D],
+ * W2 bf16 [D,hidden]; D = 384 only (VPE_E_SHAPE otherwise) */
+int vpe_op_mlp(const void* X, int32_t M, int32_t D, int32_t hidden, const void* W1, const float* b1, const void* W2,
+               const float* b2, const float* ls2, float* resid, void* stream);
 int vpe_op_attention(const void* qkv, void* out, int32_t B, int32_t T, int32_t D, int32_t heads, void* stream);
 int vpe_op_layernorm(const float* x, int32_t M, int32_t D, const float* w, const float* b, float eps, void* out_bf16,
                      const float* w2, const float* b2, void* out2_bf16, void* stream);
@@ -290,6 +294,7 @@ const char* vpe_status_str(int status);
    ((code, clock64) pairs; see csrc/attention.cu) */
 int vpe_debug_att_trace(unsigned long long* host, int32_t n);
 int vpe_debug_gemm_trace(unsigned long long* host, int32_t n);
+int vpe_debug_mlp_trace(unsigned long long* host, int32_t n);
 
 #ifdef __cplusplus
 }

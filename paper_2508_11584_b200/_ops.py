@@ -67,3 +67,12 @@ def camera_im2col(frames_hwc: torch.Tensor, resolution: int, stream=None) -> tor
     out = torch.empty(n, 640, device=frames_hwc.device, dtype=torch.bfloat16)
     check(lib.vpe_op_camera_im2col(_p(frames_hwc), B, H, W, resolution, _p(out), _s(stream)), "vpe_op_camera_im2col")
     return out
+
+
+def mlp(x: torch.Tensor, w1: torch.Tensor, b1: torch.Tensor, w2: torch.Tensor, b2: torch.Tensor,
+        ls2: torch.Tensor, resid: torch.Tensor, stream=None) -> torch.Tensor:
+    """Fused MLP block, in place: resid += ls2 * (GELU(x w1^T + b1) w2^T + b2)."""
+    M, D = x.shape
+    check(lib.vpe_op_mlp(_p(x), M, D, w1.shape[0], _p(w1), _p(b1), _p(w2), _p(b2), _p(ls2), _p(resid), _s(stream)),
+          "vpe_op_mlp")
+    return resid

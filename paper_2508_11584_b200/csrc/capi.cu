@@ -4,6 +4,7 @@
 #include <new>
 
 #include "attention.cuh"
+#include "mlp.cuh"
 #include "gemm.cuh"
 #include "misc.cuh"
 #include "runtime.h"
@@ -110,6 +111,16 @@ int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32
     VPE_TRY(plan_gemm_conv(&g, static_cast<const __nv_bfloat16*>(x), B, H, W, C, Cp, (int64_t)W * Cp,
                            (int64_t)H * W * Cp, ks, bk, static_cast<const __nv_bfloat16*>(w), N, kb, kb, ep, bn));
   VPE_TRY(launch_gemm(g, static_cast<cudaStream_t>(stream)));
+  count_launches(1);
+  return VPE_OK;
+}
+
+int vpe_op_mlp(const void* X, int32_t M, int32_t D, int32_t hidden, const void* W1, const float* b1, const void* W2,
+               const float* b2, const float* ls2, float* resid, void* stream) {
+  MlpPlan m;
+  VPE_TRY(plan_mlp(&m, static_cast<const __nv_bfloat16*>(X), M, D, hidden, static_cast<const __nv_bfloat16*>(W1), b1,
+                   static_cast<const __nv_bfloat16*>(W2), b2, ls2, resid));
+  VPE_TRY(launch_mlp(m, static_cast<cudaStream_t>(stream)));
   count_launches(1);
   return VPE_OK;
 }

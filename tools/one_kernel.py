@@ -11,7 +11,7 @@ from paper_2508_11584_b200 import _ops
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("what", choices=["attention", "gemm"])
+    p.add_argument("what", choices=["attention", "gemm", "mlp"])
     p.add_argument("--B", type=int, default=16)
     p.add_argument("--T", type=int, default=1025)
     p.add_argument("--H", type=int, default=6)
@@ -21,12 +21,21 @@ def main():
     p.add_argument("--act", type=int, default=1)
     p.add_argument("--bn", type=int, default=128)
     p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--time", action="store_true")
     a = p.parse_args()
     dev = torch.device("cuda")
     if a.what == "attention":
         D = a.H * 64
         qkv = torch.randn(a.B * a.T, 3 * D, device=dev).to(torch.bfloat16)
         fn = lambda: _ops.attention(qkv, a.B, a.T, D, a.H)
+    elif a.what == "mlp":
+        D, Hd = 384, 1536
+        x = torch.randn(a.M, D, device=dev).to(torch.bfloat16)
+        w1 = (torch.randn(Hd, D, device=dev) * 0.05).to(torch.bfloat16)
+        w2 = (torch.randn(D, Hd, device=dev) * 0.03).to(torch.bfloat16)
+        b1, b2, ls2 = torch.zeros(Hd, device=dev), torch.zeros(D, device=dev), torch.ones(D, device=dev)
+        resid = torch.zeros(a.M, D, device=dev)
+        fn = lambda: _ops.mlp(x, w1, b1, w2, b2, ls2, resid)
     else:
         x = torch.randn(a.M, a.K, device=dev).to(torch.bfloat16)
         w = (torch.randn(a.N, a.K, device=dev) * 0.02).to(torch.bfloat16)
@@ -36,6 +45,14 @@ def main():
     for _ in range(a.reps):
         fn()
     torch.cuda.synchronize()
+    if a.time:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(50):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        print(a.what, "us", e0.elapsed_time(e1) / 50 * 1e3)
 
 
 if __name__ == "__main__":
