@@ -34,6 +34,16 @@ L2_BYTES = 126 * 1024 * 1024
 BACKBONE_BN = 256  # csrc/vit.cu pick_bn() at the bench shapes
 
 
+def workload_name(args) -> str:
+    if args.model == "vits14" and args.resolution == 448 and not args.rates:
+        return "C2: DINOv2 ViT-S/14 + depth + seg + det heads, 448x448, all heads every frame"
+    name = {"vits14": "ViT-S/14", "vitb14": "ViT-B/14", "vitl14": "ViT-L/14"}.get(args.model, args.model)
+    rates = f", head rates {args.rates}" if args.rates else ", all heads every frame"
+    tag = "C3: " if args.model == "vitb14" and args.resolution == 518 and args.rates else (
+        "C5: " if args.model == "vitl14" and args.resolution == 518 else "")
+    return f"{tag}DINOv2 {name} + depth + seg + det heads, {args.resolution}x{args.resolution}{rates}"
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -45,6 +55,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--rates", default="", help="per-head frame ratios, e.g. depth=1:1,seg=1:2,det=1:4 (config C3)")
     return p.parse_args()
 
 
@@ -260,7 +271,8 @@ def run_ours(args):
     cfg = model_config(args.model)
     W = make_weights(args.model)
     B, R = args.batch, args.resolution
-    eng = VPEngine(args.model, R, B, device=local, weights=W)
+    rates = dict(kv.split("=") for kv in args.rates.split(",") if kv) if args.rates else None
+    eng = VPEngine(args.model, R, B, device=local, weights=W, rates=rates)
     # input pool larger than L2, cycled: distinct frames every step (camera stream ids sharded by rank)
     frame_bytes = B * 3 * R * R
     npool = max(4, (2 * L2_BYTES) // frame_bytes + 1)
@@ -340,8 +352,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "C2: DINOv2 ViT-S/14 + depth + seg + det heads, 448x448, all heads every frame",
-                       "model": "dinov2_vits14+dpt+linseg+rpn (random init, seeded)", "resolution": R,
+            "config": {"workload": workload_name(args),
+                       "model": f"dinov2_{args.model}+dpt+linseg+rpn (random init, seeded)", "resolution": R,
                        "batch_per_gpu": B, "camera_streams_per_gpu": B, "global_batch": B * world,
                        "parallelism": f"replicas x{world} (streams sharded, no collective)",
                        "l2": f"input pool {npool * frame_bytes / 2**20:.0f} MiB > 126 MiB L2, cycled",
