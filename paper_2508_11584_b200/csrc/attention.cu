@@ -213,9 +213,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint64_t* v_empty = v_full + VS;  // [VS]  released by both MMA issuers
   uint64_t* s_full = v_empty + VS;  // [2]
   uint64_t* s_free = s_full + 2;    // [2] softmax x has pulled S_x into registers
-  uint64_t* p_full = s_free + 2;    // [2]
-  uint64_t* o_done = p_full + 2;    // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* p_full = s_free + 2;    // [2 slots][2 key halves]
+  uint64_t* o_done = p_full + 4;    // [2 slots][2 key halves]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 4);
 
   const int BH = B * heads;
   const int npairs = (T + 255) / 256;
@@ -232,8 +232,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 8);
-      mbar_init(&p_full[i], 8);
-      mbar_init(&o_done[i], 1);
+      for (int h = 0; h < 2; ++h) {
+        mbar_init(&p_full[i * 2 + h], 4);
+        mbar_init(&o_done[i * 2 + h], 1);
+      }
     }
     for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
@@ -324,15 +326,19 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
               tc_fence_after();
               issue_s(smem_u32(sK + ks * TILE));
             }
-            mbar_wait(&p_full[x], np & 1);  // P_x(j) in TMEM
-            tc_fence_after();
-            ++np;
+            // O_x += P_x(j) V_j in two key halves, each as soon as its softmax warp pair has
+            // written its half of P (and each half of P is released on its own)
             const uint32_t v_addr = smem_u32(sV + vs * TILE);
+            for (int h = 0; h < 2; ++h) {
+              mbar_wait(&p_full[x * 2 + h], np & 1);
+              tc_fence_after();
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-              umma_f16_ts(o_t, p_t + k * 8, smem_desc(v_addr + k * 2048, 1024, 1024, 2), idesc_o,
-                          (j > 0 || k > 0) ? 1u : 0u);
-            umma_commit(&o_done[x]);
+              for (int k = 4 * h; k < 4 * h + 4; ++k)
+                umma_f16_ts(o_t, p_t + k * 8, smem_desc(v_addr + k * 2048, 1024, 1024, 2), idesc_o,
+                            (j > 0 || k > 0) ? 1u : 0u);
+              umma_commit(&o_done[x * 2 + h]);
+            }
+            ++np;
             if (next || nkv == 1) umma_commit(&k_empty[ks]);
             umma_commit(&v_empty[vs]);
             if (!next) umma_commit(&q_empty[qi]);  // every S_x of the unit issued
@@ -415,9 +421,9 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             l *= alpha;
             m_used = m_new;
           }
-          // P_x(j-1) must have been consumed (and O_x settled) before P_x(j) / the O rescale
+          // this half of P_x(j-1) must have been consumed before this half of P_x(j) is written
           if (npv > 0) {
-            mbar_wait(&o_done[x], (npv - 1) & 1);
+            mbar_wait(&o_done[x * 2 + hh], (npv - 1) & 1);
             tc_fence_after();
           }
           if (tr) ATT_TRACE(tbase, tn, 12);
@@ -440,16 +446,26 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
               tmem_st16u(p_addr + c * 16, pk);
             }
           }
-          if (rescale && j > 0 && hh == 0) {  // O_x *= alpha in TMEM, done once per row (half 0)
+          if (rescale && j > 0) {
+            // O_x *= alpha in TMEM, once per row (half 0), after both halves of PV_x(j-1) and
+            // before either half of PV_x(j) may be issued (the pair syncs before p_full)
+            mbar_wait(&o_done[x * 2 + (hh ^ 1)], (npv - 1) & 1);
+            tc_fence_after();
+            if (hh == 0) {
 #pragma unroll 1
-            for (int c = 0; c < 2; ++c) {
-              float t[32];
-              tmem_ld32(o_addr + c * 32, t);
-              tmem_ld_wait_dep(t);
+              for (int c = 0; c < 2; ++c) {
+                float t[32];
+                tmem_ld32(o_addr + c * 32, t);
+                tmem_ld_wait_dep(t);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) t[i] *= alpha;
-              tmem_st32(o_addr + c * 32, t);
+                for (int i = 0; i < 32; ++i) t[i] *= alpha;
+                tmem_st32(o_addr + c * 32, t);
+              }
+              tmem_st_wait();
             }
+            tc_fence_before();
+            pair_sync();
+            tc_fence_after();
           }
           float l0, l1;
           f2_unpack(lt, l0, l1);
@@ -461,10 +477,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (tr) ATT_TRACE(tbase, tn, 13);
-        if (lane == 0) mbar_arrive(&p_full[x]);  // this half of P_x(j) in TMEM
+        if (lane == 0) mbar_arrive(&p_full[x * 2 + hh]);  // this half of P_x(j) in TMEM
       }
       // epilogue: l = l_half0 + l_half1; each half writes 32 of the 64 output columns
-      mbar_wait(&o_done[x], (npv - 1) & 1);
+      mbar_wait(&o_done[x * 2], (npv - 1) & 1);
+      mbar_wait(&o_done[x * 2 + 1], (npv - 1) & 1);
       tc_fence_after();
       if (warp_active) {
         float* xrow = xch + ((x * 3 + 2) * 2) * 128;  // own slot: the next tile's max exchange may start

@@ -131,6 +131,25 @@ def test_attention(ops, device, B, T, heads):
     assert rel_l2(out, ref) < 1.5e-2
 
 
+@pytest.mark.parametrize("B,T,heads", [(2, 1025, 6), (1, 1370, 12)])
+def test_attention_rising_scores(ops, device, B, T, heads):
+    """Scores that rise along the key axis by more than the kernel's rescale threshold per KV tile,
+    so the running offset moves and O is rescaled in TMEM on every tile (the rare path)."""
+    D = heads * 64
+    g = torch.Generator().manual_seed(T + 1)
+    qkv = torch.randn(B * T, 3 * D, generator=g) * 0.3
+    ramp = torch.linspace(0, 10, T).repeat(B)                   # key t gets + ramp[t] per dim
+    qkv[:, :D] += 1.0                                           # q . k ~ 64 * ramp -> s/8 ~ 8 * ramp
+    qkv[:, D:2 * D] += ramp[:, None]
+    qkv = qkv.to(device, torch.bfloat16)
+    out = ops.attention(qkv, B, T, D, heads)
+    q, k, v = qkv.float().view(B, T, 3, heads, 64).permute(2, 0, 3, 1, 4)
+    ref = torch.softmax(q @ k.transpose(-1, -2) / 8.0, -1) @ v
+    ref = ref.transpose(1, 2).reshape(B * T, D)
+    torch.cuda.synchronize()
+    assert rel_l2(out, ref) < 1.5e-2
+
+
 def test_layernorm(ops, device):
     g = torch.Generator().manual_seed(3)
     x = (torch.randn(1025, 384, generator=g) * 3 + 1).to(device)
