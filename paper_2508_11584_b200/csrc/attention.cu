@@ -23,7 +23,12 @@
 // 32 rows are all past T skip the exponentials.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <tuple>
+#include <utility>
+#include <vector>
 
 #include "attention.cuh"
 #include "tc.cuh"
@@ -197,7 +202,7 @@ VPE_DEV AttnUnit unit_of(int u, int BH, int heads, int T) {
 template <int POLY>
 __global__ void __launch_bounds__(ATT_THREADS, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tqkv, __nv_bfloat16* __restrict__ out, int B, int T,
-                        int D, int heads, float scale_log2, int trace) {
+                        int D, int heads, float scale_log2, int trace, const int* __restrict__ sched) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;               // [2 units][2 slots]: the next unit's Q lands during this one
@@ -218,9 +223,10 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 4);
 
   const int BH = B * heads;
-  const int npairs = (T + 255) / 256;
-  const int units = BH * npairs;
   const int nkv = (T + 127) / 128;
+  // this CTA's units (host LPT schedule, heavy first, so units without a B tile come last)
+  const int u_lo = __ldg(sched + blockIdx.x), u_hi = __ldg(sched + blockIdx.x + 1);
+  const int* ulist = sched + gridDim.x + 1;
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (warp == 0 && lane == 0) {
@@ -258,8 +264,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {
       int kit = 0, vit = 0, qn = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++qn) {
-        const AttnUnit w = unit_of(u, BH, heads, T);
+      for (int ui = u_lo; ui < u_hi; ++ui, ++qn) {
+        const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T);
         const int row0 = w.b * T;
         const int qb = qn & 1;
         for (int x = 0; x < 1 + w.has_b; ++x) {
@@ -286,8 +292,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       constexpr uint32_t idesc_o = idesc_bf16(128, 64, /*b_mn_major=*/true);
       int kit = 0, vit = 0, qn = 0, np = 0;  // np: PV MMAs issued (= p_full / s_free phases consumed)
       const uint32_t s_t = tmem + S_COL + x * 128, p_t = tmem + P_COL + x * 64, o_t = tmem + O_COL + x * 64;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++qn) {
-        const AttnUnit w = unit_of(u, BH, heads, T);
+      for (int ui = u_lo; ui < u_hi; ++ui, ++qn) {
+        const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T);
         const bool mine = (x == 0) || w.has_b;
         const int qi = (qn & 1) * 2 + x;
         if (mine) {
@@ -370,8 +376,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     const bool tr = (quad == 0 && lane == 0 && hh == 0);
     const int tbase = 2048 + 1024 * x;
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const AttnUnit w = unit_of(u, BH, heads, T);
+    for (int ui = u_lo; ui < u_hi; ++ui) {
+      const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T);
       if (x == 1 && !w.has_b) continue;
       const int q0 = w.q0 + x * 128;
       const bool warp_active = (q0 + quad * 32) < T;
@@ -532,10 +538,51 @@ int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, in
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int units = B * heads * ((T + 255) / 256);
+  const int BH = B * heads, npairs = (T + 255) / 256, units = BH * npairs;
   a->grid = units < sms ? units : sms;
   const char* e = getenv("VPE_ATT_GRID");  // experiment: "all" = one unit per CTA (no persistence)
   if (e && e[0] == 'a') a->grid = units;
+  // Longest-processing-time-first static schedule: a unit costs ~ its Q tiles' valid rows plus a
+  // fixed MMA/pipeline share; heavy units first, each to the least-loaded CTA. Round-robin left
+  // T = 1025 at 3 full pairs + 1 tail unit on 36 CTAs (the tail pair holds one valid row).
+  static std::map<std::tuple<int, int, int, int>, int*> cache;  // (B*heads, T, grid) -> device schedule
+  const auto key = std::make_tuple(BH, T, a->grid, 0);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    std::vector<std::pair<double, int>> cost(units);
+    for (int u = 0; u < units; ++u) {
+      const int q0 = (u / BH) * 256;
+      double c = 0;
+      for (int t = 0; t < 2; ++t) {
+        const int rows = std::min(128, std::max(0, T - (q0 + 128 * t)));
+        if (rows > 0) c += 0.35 + 0.65 * rows / 128.0;
+      }
+      cost[u] = {c, u};
+    }
+    std::stable_sort(cost.begin(), cost.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<double> load(a->grid, 0.0);
+    std::vector<std::vector<int>> lists(a->grid);
+    for (const auto& cu : cost) {
+      int best = 0;
+      for (int c = 1; c < a->grid; ++c)
+        if (load[c] < load[best]) best = c;
+      load[best] += cu.first;
+      lists[best].push_back(cu.second);
+    }
+    std::vector<int> host(a->grid + 1 + units);
+    int off = 0;
+    for (int c = 0; c < a->grid; ++c) {
+      host[c] = off;
+      for (int u : lists[c]) host[a->grid + 1 + off++] = u;
+    }
+    host[a->grid] = off;
+    int* d = nullptr;
+    if (cudaMalloc(&d, host.size() * sizeof(int)) != cudaSuccess) return VPE_E_RESOURCE;
+    if (cudaMemcpy(d, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess)
+      return VPE_E_CUDA;
+    it = cache.emplace(key, d).first;
+  }
+  a->sched = it->second;
   return VPE_OK;
 }
 
@@ -557,7 +604,8 @@ int launch_attention(const AttnPlan& a, cudaStream_t s) {
   auto k = poly == 0 ? attention_tc_kernel<0>
                      : (poly == 2 ? attention_tc_kernel<0x0303>
                                   : (poly == 3 ? attention_tc_kernel<0x1111> : attention_tc_kernel<0x0707>));
-  k<<<a.grid, ATT_THREADS, SMEM_ATT, s>>>(a.tqkv, a.out, a.B, a.T, a.D, a.heads, scale_log2, g_att_trace_on);
+  k<<<a.grid, ATT_THREADS, SMEM_ATT, s>>>(a.tqkv, a.out, a.B, a.T, a.D, a.heads, scale_log2, g_att_trace_on,
+                                          a.sched);
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
 }
 
