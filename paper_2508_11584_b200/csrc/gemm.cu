@@ -861,7 +861,7 @@ int encode_tma(CUtensorMap* m, int rank, const void* ptr, const uint64_t* dims, 
 static int smem_for(int bn, int bk) {
 #define VPE_SM(BN_, BK_) \
   if (bn == BN_ && bk == BK_) return (int)GemmCfg<BN_, BK_>::SMEM;
-  VPE_SM(32, 64) VPE_SM(64, 64) VPE_SM(128, 64) VPE_SM(256, 64) VPE_SM(32, 32) VPE_SM(64, 32)
+  VPE_SM(32, 64) VPE_SM(64, 64) VPE_SM(128, 64) VPE_SM(192, 64) VPE_SM(256, 64) VPE_SM(32, 32) VPE_SM(64, 32)
 #undef VPE_SM
   return -1;
 }
@@ -1186,7 +1186,7 @@ int launch_gemm(const GemmPlan& g, cudaStream_t s) {
   }
 #define VPE_L(BN_, BK_) \
   if (g.bn == BN_ && g.bk == BK_) return launch_t<BN_, BK_>(g, s);
-  VPE_L(32, 64) VPE_L(64, 64) VPE_L(128, 64) VPE_L(256, 64) VPE_L(32, 32) VPE_L(64, 32)
+  VPE_L(32, 64) VPE_L(64, 64) VPE_L(128, 64) VPE_L(192, 64) VPE_L(256, 64) VPE_L(32, 32) VPE_L(64, 32)
 #undef VPE_L
   return VPE_E_SHAPE;
 }

@@ -38,7 +38,7 @@ def main():
         bias = torch.zeros(N, device=dev)
         out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
         outf = torch.empty(M, N, device=dev, dtype=torch.float32)
-        for bn in (128, 256, -128, -192, -256):
+        for bn in (128, 192, 256):
             for act in (0, 1):
                 us = timeit(lambda: _ops.linear(a, w, bias=bias, out=out, act=act, bn=bn))
                 tf = 2 * M * N * K / us * 1e-6
