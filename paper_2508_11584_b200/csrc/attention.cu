@@ -258,6 +258,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();
+  pdl_trigger();
 
   // Units are ordered pair-major, so a unit without a B tile (T <= q0 + 128) is followed only by
   // such units: the slot-B barriers are simply left alone from then on.
@@ -604,9 +606,10 @@ int launch_attention(const AttnPlan& a, cudaStream_t s) {
   auto k = poly == 0 ? attention_tc_kernel<0>
                      : (poly == 2 ? attention_tc_kernel<0x0303>
                                   : (poly == 3 ? attention_tc_kernel<0x1111> : attention_tc_kernel<0x0707>));
-  k<<<a.grid, ATT_THREADS, SMEM_ATT, s>>>(a.tqkv, a.out, a.B, a.T, a.D, a.heads, scale_log2, g_att_trace_on,
-                                          a.sched);
-  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+  return launch_k(k, dim3(a.grid), dim3(ATT_THREADS), SMEM_ATT, s, a.tqkv, a.out, a.B, a.T, a.D, a.heads, scale_log2,
+                  g_att_trace_on, a.sched) == cudaSuccess
+             ? VPE_OK
+             : VPE_E_CUDA;
 }
 
 }  // namespace vpe

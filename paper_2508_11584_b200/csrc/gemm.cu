@@ -333,6 +333,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();
+  pdl_trigger();
   const int ntiles = p.m_tiles * p.n_tiles;
 
   if (warp == 0) {
@@ -523,6 +525,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   cluster_sync();  // the peer's barriers are initialised before anything can signal them
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();
+  pdl_trigger();
   const int ntiles = p.m_tiles * p.n_tiles;  // m_tiles counts 256-row pairs
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
 
@@ -692,6 +696,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  pdl_wait();
+  pdl_trigger();
   const int ntiles = p.m_tiles * p.n_tiles;
   const int groups = p.cchunks;  // channel groups of GCH
 
@@ -1128,8 +1134,9 @@ static int launch_halo_t(const GemmPlan& g, cudaStream_t s) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg<BN, KC, RT, WRES>::SMEM);
     attr_set = true;
   }
-  k<<<g.grid, GEMM_THREADS, HaloCfg<BN, KC, RT, WRES>::SMEM, s>>>(g.ta, g.tb, g.p);
-  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+  return launch_k(k, g.grid, dim3(GEMM_THREADS), HaloCfg<BN, KC, RT, WRES>::SMEM, s, g.ta, g.tb, g.p) == cudaSuccess
+             ? VPE_OK
+             : VPE_E_CUDA;
 }
 
 template <int BN, int BK>
@@ -1146,8 +1153,9 @@ static int launch_t(const GemmPlan& g, cudaStream_t s) {
   }
   GemmParams p = g.p;
   p.trace = g_gemm_trace_on;
-  k<<<g.grid, GEMM_THREADS, GemmCfg<BN, BK>::SMEM, s>>>(g.ta, g.tb, g.tout, p);
-  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+  return launch_k(k, g.grid, dim3(GEMM_THREADS), GemmCfg<BN, BK>::SMEM, s, g.ta, g.tb, g.tout, p) == cudaSuccess
+             ? VPE_OK
+             : VPE_E_CUDA;
 }
 
 template <int BN>

@@ -17,6 +17,8 @@ namespace vpe {
 // Also writes the cls rows of the fp32 residual stream: h[b*T] = cls_token + pos[0].
 __global__ void patch_im2col_kernel(const uint8_t* __restrict__ px, __nv_bfloat16* __restrict__ A, int B, int R,
                                     int KP, float* __restrict__ resid, const float* __restrict__ cls_pos0, int D) {
+  pdl_wait();
+  pdl_trigger();
   const int h = R / 14, np = h * h;
   const int blk = blockIdx.x;
   if (blk >= B * np) {
@@ -44,8 +46,10 @@ __global__ void patch_im2col_kernel(const uint8_t* __restrict__ px, __nv_bfloat1
 int launch_patch_im2col(const uint8_t* px, __nv_bfloat16* A, int B, int R, int KP, float* resid,
                         const float* cls_pos0, int D, cudaStream_t s) {
   const int np = (R / 14) * (R / 14);
-  patch_im2col_kernel<<<B * np + B, 128, 0, s>>>(px, A, B, R, KP, resid, cls_pos0, D);
-  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+  return launch_k(patch_im2col_kernel, dim3(B * np + B), dim3(128), 0, s, px, A, B, R, KP, resid, cls_pos0, D) ==
+                 cudaSuccess
+             ? VPE_OK
+             : VPE_E_CUDA;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -56,6 +60,8 @@ int launch_patch_im2col(const uint8_t* px, __nv_bfloat16* A, int B, int R, int K
 __global__ void camera_im2col_kernel(const uint8_t* __restrict__ hwc, int Hc, int Wc, __nv_bfloat16* __restrict__ A,
                                      int B, int R, int KP, float* __restrict__ resid,
                                      const float* __restrict__ cls_pos0, int D) {
+  pdl_wait();
+  pdl_trigger();
   const int h = R / 14, np = h * h;
   const int blk = blockIdx.x;
   if (blk >= B * np) {
@@ -98,8 +104,10 @@ int launch_camera_im2col(const uint8_t* hwc, int Hc, int Wc, __nv_bfloat16* A, i
                          const float* cls_pos0, int D, cudaStream_t s) {
   if (Hc < 1 || Wc < 1 || R % 14) return VPE_E_SHAPE;
   const int np = (R / 14) * (R / 14);
-  camera_im2col_kernel<<<B * np + B, 128, 0, s>>>(hwc, Hc, Wc, A, B, R, KP, resid, cls_pos0, D);
-  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+  return launch_k(camera_im2col_kernel, dim3(B * np + B), dim3(128), 0, s, hwc, Hc, Wc, A, B, R, KP, resid, cls_pos0,
+                  D) == cudaSuccess
+             ? VPE_OK
+             : VPE_E_CUDA;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -110,6 +118,8 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int M, int D, cons
                                  const float* __restrict__ b, float eps, __nv_bfloat16* __restrict__ out,
                                  const float* __restrict__ w2, const float* __restrict__ b2,
                                  __nv_bfloat16* __restrict__ out2) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -164,7 +174,10 @@ int launch_layernorm(const float* x, int M, int D, const float* w, const float* 
   dim3 grid((M + rows_per_block - 1) / rows_per_block), block(32 * rows_per_block);
   switch (D / 128) {
 #define VPE_LN(NV_) \
-  case NV_: layernorm_kernel<NV_><<<grid, block, 0, s>>>(x, M, D, w, b, eps, out, w2, b2, out2); break;
+  case NV_:                                                                                         \
+    if (launch_k(layernorm_kernel<NV_>, grid, block, 0, s, x, M, D, w, b, eps, out, w2, b2, out2) != cudaSuccess) \
+      return VPE_E_CUDA;                                                                             \
+    break;
     VPE_LN(1) VPE_LN(2) VPE_LN(3) VPE_LN(4) VPE_LN(5) VPE_LN(6) VPE_LN(8) VPE_LN(10) VPE_LN(12)
 #undef VPE_LN
     default:

@@ -26,6 +26,15 @@ VPE_DEV bool elect_one() {
   return pred != 0;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Backbone kernels are launched through launch_k, which can add programmatic stream
+// serialization (VPE_PDL=1): the next kernel in the stream may then start its prologue (barrier
+// init, TMEM alloc, descriptor prefetch) while this one drains. pdl_wait() blocks until the previous grid has completed and its
+// memory is visible, so each kernel calls it before its first dependent global access;
+// pdl_trigger() lets the dependent grid be scheduled as early as resources allow.
+VPE_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+VPE_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- mbarrier
 VPE_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
