@@ -79,21 +79,23 @@ __global__ void k(const __grid_constant__ CUtensorMap ta, const __grid_constant_
     mbar_wait(&done, 0);
     out[blockIdx.x] = clock64() - t0;
     stop_flag = 1;
-  } else if (warp >= 4 && epi == 2) {
-    // fake epilogue: 2 KB bulk stores smem -> global from each warp (TMA store path), 1 in flight
-    if (lane == 0) {
+  } else if (warp >= 4 && (epi == 2 || epi == 3)) {
+    // fake epilogue: bulk stores smem -> global (TMA store path), 1 in flight per warp;
+    // epi 2: 2 KB from each of 8 warps; epi 3: 16 KB from one warp
+    if (lane == 0 && (epi == 2 || warp == 4)) {
+      const int sz = epi == 2 ? 2048 : 16384;
       char* dst = reinterpret_cast<char*>(gout) + ((size_t)blockIdx.x * 8 + (warp - 4)) * 2048 * 64;
-      const uint32_t src = smem_u32(s);  // any 2 KB of smem
+      const uint32_t src = smem_u32(s);  // any bytes of smem
       int n = 0;
       while (!stop_flag) {
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 2048;" ::"l"(dst + (n & 63) * 2048), "r"(src) : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + (size_t)(n & 7) * sz), "r"(src), "r"(sz) : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         ++n;
         for (int sp = 0; sp < throttle; ++sp) __nanosleep(32);
       }
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      out[148 + blockIdx.x * 8 + warp - 4] = n;
+      out[148 + blockIdx.x * 8 + warp - 4] = (unsigned long long)n * (sz / 2048);
     }
   } else if (warp >= 4 && epi) {
     // fake epilogue: tcgen05.ld 32x32b.x32 from the OTHER accumulator half (cols 256..511)
@@ -144,7 +146,7 @@ void run(unsigned long long* d, CUtensorMap ta, CUtensorMap tb, int epi = 0, int
   unsigned long long mx = 0, sum = 0;
   for (int i = 0; i < 148; ++i) { mx = h[i] > mx ? h[i] : mx; sum += h[i]; }
   unsigned long long nst = 0;
-  if (epi == 2) for (int i = 0; i < 148 * 8; ++i) nst += h[148 + i];
+  if (epi >= 2) for (int i = 0; i < 148 * 8; ++i) nst += h[148 + i];
   printf("stores/SM=%.0f (%.1f B/clk/SM)  ", nst / 148.0, nst / 148.0 * 2048 / ((double)sum / 148));
   printf("epi=%d stages=%d BN=%d  clk/kblock mean=%.1f max=%.1f (ideal %d)  (%s)\n", epi, S, BN, (double)sum / 148 / iters,
          (double)mx / iters, BN * 2, cudaGetErrorString(cudaGetLastError()));
@@ -169,5 +171,8 @@ int main() {
   run<4, 256>(d, ta, tb, 2, 0);
   run<4, 256>(d, ta, tb, 2, 4);
   run<4, 256>(d, ta, tb, 2, 16);
+  run<4, 256>(d, ta, tb, 3, 0);
+  run<4, 256>(d, ta, tb, 3, 16);
+  run<4, 256>(d, ta, tb, 3, 64);
   return 0;
 }
