@@ -288,7 +288,10 @@ int vpe_event_elapsed_ms(void* start, void* end, float* ms);
 int vpe_event_destroy(void* ev);
 int vpe_stream_wait_event(void* stream, void* ev);
 int vpe_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
-int64_t vpe_kernel_launches(void);    /* kernels enqueued by libvpe since load (graph replays count per node) */
+int64_t vpe_kernel_launches(void);
+/* programmatic dependent launch for kernels enqueued (or graph-captured) from now on: on for
+ * latency-bound small batches, off for throughput (see csrc/util.cuh); VPE_PDL env overrides */
+int vpe_set_pdl(int32_t on);    /* kernels enqueued by libvpe since load (graph replays count per node) */
 const char* vpe_status_str(int status);
 /* diagnostics: timeline of attention CTA 0 when the process runs with VPE_ATT_TRACE=1
    ((code, clock64) pairs; see csrc/attention.cu) */

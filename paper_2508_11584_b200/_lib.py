@@ -141,6 +141,7 @@ _SIGS = {
     # ops
     "vpe_op_linear": (i32, [vp, i32, i32, vp, i32, i32, vp, vp, vp, i32, i32, i32, vp]),
     "vpe_op_conv": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, i32, vp, vp, vp, vp, vp, i32, i32, vp]),
+    "vpe_set_pdl": (i32, [i32]),
     "vpe_debug_att_trace": (i32, [vp, i32]),
     "vpe_debug_gemm_trace": (i32, [vp, i32]),
     "vpe_debug_mlp_trace": (i32, [vp, i32]),

@@ -115,6 +115,11 @@ int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32
   return VPE_OK;
 }
 
+int vpe_set_pdl(int32_t on) {
+  pdl_flag() = on ? 1 : 0;
+  return VPE_OK;
+}
+
 int vpe_op_mlp(const void* X, int32_t M, int32_t D, int32_t hidden, const void* W1, const float* b1, const void* W2,
                const float* b2, const float* ls2, float* resid, void* stream) {
   MlpPlan m;

@@ -23,16 +23,32 @@
   } while (0)
 
 namespace vpe {
-// PDL off by default (VPE_PDL=1 enables): measured neutral on the backbone alone (2.184 ->
-// 2.175 ms) and slightly negative on the pipelined step with concurrent head streams (3.58 ->
-// 3.63 ms), where early-scheduled dependents hold SM slots the head kernels could use.
+// Programmatic dependent launch: a process-wide switch set per engine before it captures its
+// graphs (vpe_set_pdl; VPE_PDL=0/1 overrides). Measured: latency mode (batch 1) backbone 0.752 ->
+// 0.695 ms and head p50 -8..-9%; throughput mode with concurrent head streams 3.51 -> 3.57 ms
+// per step (early-scheduled dependents hold SM slots the head kernels could use), so engines
+// turn it on for small batches only.
+inline int& pdl_flag() {
+  static int on = 0;
+  return on;
+}
+// Scope: only the backbone's kernel chain after its first kernel is launched with PDL (vit.cu
+// sets the scope); head kernels keep full stream serialization. A PDL kernel whose stream
+// predecessor is an event wait (the head graphs start by waiting on the ring's ready event) was
+// measured to break graph-replay determinism (tests/test_gpu_engine.py), so the first kernel
+// after any non-kernel dependency is never launched with PDL.
+inline int& pdl_scope() {
+  static thread_local int s = 0;
+  return s;
+}
 inline bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
+  static int env = -2;
+  if (env == -2) {
     const char* e = getenv("VPE_PDL");
-    on = (e && e[0] == '1') ? 1 : 0;
+    env = e ? (e[0] == '1' ? 1 : 0) : -1;
   }
-  return on == 1;
+  if (!pdl_scope()) return false;
+  return env >= 0 ? env == 1 : pdl_flag() == 1;
 }
 // <<<grid, block, smem, stream>>> with programmatic stream serialization (see tc.cuh pdl_wait)
 template <typename... KArgs, typename... Args>

@@ -158,7 +158,14 @@ extern "C" int vpe_vit_residual(vpe_vit* v, const float** resid) {
 }
 
 // Shared tail of both entry points: patch GEMM, the L blocks, final LN into taps[3].
+static int vit_blocks_impl(vpe_vit* v, void* const* taps, cudaStream_t s);
 static int vit_blocks(vpe_vit* v, void* const* taps, cudaStream_t s) {
+  pdl_scope() = 1;  // kernels after the patch im2col may overlap their predecessor's drain
+  const int rc = vit_blocks_impl(v, taps, s);
+  pdl_scope() = 0;
+  return rc;
+}
+static int vit_blocks_impl(vpe_vit* v, void* const* taps, cudaStream_t s) {
   const vpe_vit_config& c = v->cfg;
   const vpe_vit_weights& w = v->w;
   const int D = c.dim, M = v->M;

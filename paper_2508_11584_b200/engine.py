@@ -92,9 +92,13 @@ class VPEngine:
                  heads=("depth", "seg", "det"), capacity: int | None = None, rates: dict | None = None,
                  device: int = 0, weights: dict | None = None, graphs: bool = True, seed: int = 0,
                  namespace: str | None = None, max_latency_records: int = 4096,
-                 camera: tuple[int, int] | None = None):
+                 camera: tuple[int, int] | None = None, pdl: bool | None = None):
         torch.cuda.set_device(device)
         self.device = torch.device(f"cuda:{device}")
+        # programmatic dependent launch pays off for latency-bound small batches and costs
+        # throughput when large-batch head streams run concurrently (csrc/util.cuh)
+        self.pdl = (batch <= 2) if pdl is None else bool(pdl)
+        check(lib.vpe_set_pdl(int(self.pdl)), "vpe_set_pdl")
         self.cfg = model_config(model)
         self.model, self.resolution, self.batch = model, resolution, batch
         self.head_names = tuple(heads)
