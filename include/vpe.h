@@ -270,6 +270,11 @@ int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32
 int vpe_op_mlp(const void* X, int32_t M, int32_t D, int32_t hidden, const void* W1, const float* b1, const void* W2,
                const float* b2, const float* ls2, float* resid, void* stream);
 int vpe_op_attention(const void* qkv, void* out, int32_t B, int32_t T, int32_t D, int32_t heads, void* stream);
+/* bilinear (align_corners=False) upsample of fp32 logits [B, h*h, cp] (C real classes) to
+ * [B, R, R] + argmax over classes -> u8 labels; R = 14 h; torch's rounding and first-index ties
+ * (reference seg head: SPEC.md:232-243, oracle/seg.py seg_forward) */
+int vpe_op_upsample_argmax(const float* logits, int32_t B, int32_t h, int32_t C, int32_t cp, int32_t resolution,
+                           uint8_t* labels, void* stream);
 int vpe_op_layernorm(const float* x, int32_t M, int32_t D, const float* w, const float* b, float eps, void* out_bf16,
                      const float* w2, const float* b2, void* out2_bf16, void* stream);
 

@@ -88,6 +88,11 @@ class CpuPipeline:
 
     def close(self):
         try:
+            for _, grp in self.dst.values():  # drop the ndarray views first: they pin the mmap
+                grp._views.clear()
+                grp.arena.close()
+            self.dst.clear()
+            self.chan._group_views.clear()
             self.chan.close()
             self.chan.unlink()
             self.ar.clean_namespace(self.ns)

@@ -60,6 +60,17 @@ def layernorm(x: torch.Tensor, w, b, eps=1e-6, w2=None, b2=None, stream=None):
     return out if out2 is None else (out, out2)
 
 
+def upsample_argmax(logits: torch.Tensor, h: int, resolution: int, classes: int | None = None, stream=None):
+    """logits fp32 [B, h*h, cp] -> u8 labels [B, R, R] (bilinear align_corners=False, argmax)."""
+    B, hw, cp = logits.shape
+    assert hw == h * h and logits.dtype == torch.float32 and logits.is_contiguous()
+    C = cp if classes is None else classes
+    labels = torch.empty(B, resolution, resolution, device=logits.device, dtype=torch.uint8)
+    check(lib.vpe_op_upsample_argmax(_p(logits), B, h, C, cp, resolution, _p(labels), _s(stream)),
+          "vpe_op_upsample_argmax")
+    return labels
+
+
 def camera_im2col(frames_hwc: torch.Tensor, resolution: int, stream=None) -> torch.Tensor:
     """u8 [B,H,W,3] -> normalised bf16 patch rows [B*(R/14)^2, 640] (crop, resize, normalise fused)."""
     B, H, W, _ = frames_hwc.shape

@@ -22,6 +22,11 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-I", os.path.join(HERE, "..", "include")]
 
 
+# seg.cu: the fused upsample+argmax must round every mul and add separately (torch's order) and
+# ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 unless told not to
+EXTRA = {"seg.cu": ["--fmad=false"]}
+
+
 def _stale(src: str, obj: str) -> bool:
     if not os.path.exists(obj):
         return True
@@ -41,7 +46,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     def one(job):
         s, o = job
-        cmd = [NVCC, *FLAGS, "-c", s, "-o", o]
+        cmd = [NVCC, *FLAGS, *EXTRA.get(os.path.basename(s), []), "-c", s, "-o", o]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -8,6 +8,7 @@
 #include <new>
 
 #include "gemm.cuh"
+#include "tc.cuh"
 #include "runtime.h"
 #include "util.cuh"
 
@@ -27,7 +28,7 @@ namespace {
 // source index per torch's area_pixel_compute_source_index (align_corners=False, no cubic)
 __device__ __forceinline__ void src_index(float scale, int dst, int in_size, int& i0, int& i1, float& l0,
                                           float& l1) {
-  float s = scale * ((float)dst + 0.5f) - 0.5f;
+  float s = __fmaf_rn(scale, (float)dst + 0.5f, -0.5f);  // explicit: this file builds with --fmad=false
   if (s < 0.f) s = 0.f;
   i0 = (int)s;
   i1 = i0 + ((i0 < in_size - 1) ? 1 : 0);
@@ -38,14 +39,41 @@ __device__ __forceinline__ void src_index(float scale, int dst, int in_size, int
 // Fused bilinear (align_corners=False) upsample + argmax, torch's rounding order
 //   out = (x00*w0 + x01*w1)*h0 + (x10*w0 + x11*w1)*h1.
 // A CTA owns half a source band: the 7 output rows that all read the same two source rows, every
-// output column of them (one thread per column). Per class a thread loads the 4 corner logits
-// once, forms the two x-interpolations once and reuses them for its 7 output pixels, keeping 7
-// running (max, argmax) pairs in registers; the [C, R, R] logit volume never exists.
+// output column of them (one thread per column); the [C, R, R] logit volume never exists.
+// Instruction diet (the kernel is issue-bound): classes go two at a time through packed f32x2
+// mul/add (IEEE RN per lane, so bit-identical to the scalar formula), the x-interpolations are
+// shared by the 7 rows, and the running argmax is kept per chunk of SEG_G classes — a 3-input max
+// per class pair, one compare per chunk — with the index recovered at the end by re-evaluating
+// only the winning chunk and taking its first class equal to the maximum (torch's first-occurrence
+// tie rule: a later chunk only wins on a strictly greater maximum).
 constexpr int HALF_ROWS = 7;  // R / h / 2
+constexpr int SEG_G = 8;      // classes per argmax chunk
+
+__device__ __forceinline__ float seg_fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// a*b rounded once, as fma(a, b, z) with z a +0 pair the compiler cannot see: ptxas contracts
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under --fmad=false, which would change the rounding
+// (only the sign of an exact-zero product can differ from mul.rn, and -0 == +0 in every compare)
+__device__ __forceinline__ uint64_t seg_mul2(uint64_t a, uint64_t b, uint64_t z) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(z));
+  return d;
+}
+__device__ __forceinline__ float seg_value(const float* r0, const float* r1, int x0, int x1, int cs, int c, float wx0,
+                                           float wx1, float h0, float h1) {
+  const float t0 = __fadd_rn(__fmul_rn(r0[x0 * cs + c], wx0), __fmul_rn(r0[x1 * cs + c], wx1));
+  const float t1 = __fadd_rn(__fmul_rn(r1[x0 * cs + c], wx0), __fmul_rn(r1[x1 * cs + c], wx1));
+  return __fadd_rn(__fmul_rn(t0, h0), __fmul_rn(t1, h1));
+}
+
 __global__ void __launch_bounds__(1024)
     seg_upsample_argmax_kernel(const float* __restrict__ logits, int h, int C, int cp, int R,
-                               uint8_t* __restrict__ labels) {
-  extern __shared__ float s_src[];  // [2 rows][h cols][C]
+                               uint8_t* __restrict__ labels, float zero) {
+  extern __shared__ float s_src[];  // [2 rows][h cols][cs], cs = C rounded up to even
+  const int cs = (C + 1) & ~1;
   const int hb = blockIdx.x, b = blockIdx.y;
   const float scale = (float)h / (float)R;
   const int oy0 = hb * HALF_ROWS;
@@ -53,10 +81,15 @@ __global__ void __launch_bounds__(1024)
   float hy0_unused, hy1_unused;
   src_index(scale, oy0, h, y0, y1, hy0_unused, hy1_unused);
   const float* src = logits + (int64_t)b * h * h * cp;
-  for (int i = threadIdx.x; i < 2 * h * C; i += blockDim.x) {
-    const int c = i % C, pix = i / C;
-    const int yy = pix / h ? y1 : y0, xx = pix % h;
-    s_src[i] = src[((int64_t)yy * h + xx) * cp + c];
+  {  // stage the two source rows: one warp per source pixel, lanes across classes (no div/mod)
+    const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int pix = wid; pix < 2 * h; pix += nw) {
+      const int yy = pix < h ? y0 : y1, xx = pix < h ? pix : pix - h;
+      const float* g = src + ((int64_t)yy * h + xx) * cp;
+      float* d = s_src + pix * cs;
+#pragma unroll 4
+      for (int c = lane; c < cs; c += 32) d[c] = c < C ? __ldg(g + c) : 0.f;
+    }
   }
   __syncthreads();
   const int ox = threadIdx.x;
@@ -65,23 +98,55 @@ __global__ void __launch_bounds__(1024)
   float wx0, wx1;
   src_index(scale, ox, h, x0, x1, wx0, wx1);
   float hy0[HALF_ROWS], hy1[HALF_ROWS], best[HALF_ROWS];
+  uint64_t H0[HALF_ROWS], H1[HALF_ROWS];
   int arg[HALF_ROWS];
 #pragma unroll
   for (int k = 0; k < HALF_ROWS; ++k) {
     int a0, a1;
     src_index(scale, oy0 + k, h, a0, a1, hy0[k], hy1[k]);
+    H0[k] = f2_pack(hy0[k], hy0[k]);
+    H1[k] = f2_pack(hy1[k], hy1[k]);
     best[k] = -INFINITY;
-    arg[k] = 0;
+    arg[k] = 0;  // chunk start until the final pass
   }
+  const uint64_t W0 = f2_pack(wx0, wx0), W1 = f2_pack(wx1, wx1), Z = f2_pack(zero, zero);
   const float* r0 = s_src;
-  const float* r1 = s_src + h * C;
-#pragma unroll 2
-  for (int c = 0; c < C; ++c) {
-    const float t0 = __fadd_rn(__fmul_rn(r0[x0 * C + c], wx0), __fmul_rn(r0[x1 * C + c], wx1));
-    const float t1 = __fadd_rn(__fmul_rn(r1[x0 * C + c], wx0), __fmul_rn(r1[x1 * C + c], wx1));
+  const float* r1 = s_src + h * cs;
+  const uint64_t* p00 = reinterpret_cast<const uint64_t*>(r0 + x0 * cs);
+  const uint64_t* p01 = reinterpret_cast<const uint64_t*>(r0 + x1 * cs);
+  const uint64_t* p10 = reinterpret_cast<const uint64_t*>(r1 + x0 * cs);
+  const uint64_t* p11 = reinterpret_cast<const uint64_t*>(r1 + x1 * cs);
+  const int cg = C / SEG_G * SEG_G;
+#pragma unroll 1
+  for (int c0 = 0; c0 < cg; c0 += SEG_G) {
+    float m[HALF_ROWS];
+#pragma unroll
+    for (int k = 0; k < HALF_ROWS; ++k) m[k] = -INFINITY;
+#pragma unroll
+    for (int pc = 0; pc < SEG_G / 2; ++pc) {
+      const int q = (c0 >> 1) + pc;  // class pair (c, c + 1)
+      const uint64_t T0 = fadd2(seg_mul2(p00[q], W0, Z), seg_mul2(p01[q], W1, Z));
+      const uint64_t T1 = fadd2(seg_mul2(p10[q], W0, Z), seg_mul2(p11[q], W1, Z));
+#pragma unroll
+      for (int k = 0; k < HALF_ROWS; ++k) {
+        float va, vb;
+        f2_unpack(fadd2(seg_mul2(T0, H0[k], Z), seg_mul2(T1, H1[k], Z)), va, vb);
+        m[k] = seg_fmax3(m[k], va, vb);
+      }
+    }
 #pragma unroll
     for (int k = 0; k < HALF_ROWS; ++k) {
-      const float v = __fadd_rn(__fmul_rn(t0, hy0[k]), __fmul_rn(t1, hy1[k]));
+      if (m[k] > best[k]) {
+        best[k] = m[k];
+        arg[k] = c0;
+      }
+    }
+  }
+#pragma unroll 1
+  for (int c = cg; c < C; ++c) {  // tail classes: a chunk of one
+#pragma unroll
+    for (int k = 0; k < HALF_ROWS; ++k) {
+      const float v = seg_value(r0, r1, x0, x1, cs, c, wx0, wx1, hy0[k], hy1[k]);
       if (v > best[k]) {
         best[k] = v;
         arg[k] = c;
@@ -89,9 +154,52 @@ __global__ void __launch_bounds__(1024)
     }
   }
 #pragma unroll
-  for (int k = 0; k < HALF_ROWS; ++k) labels[((int64_t)b * R + oy0 + k) * R + ox] = (uint8_t)arg[k];
+  for (int k = 0; k < HALF_ROWS; ++k) {
+    const int c0 = arg[k];
+    if (c0 < cg) {  // winning chunk: first class of it equal to the max, two classes at a time
+#pragma unroll 1
+      for (int q = c0 >> 1; q < (c0 + SEG_G) >> 1; ++q) {
+        const uint64_t T0 = fadd2(seg_mul2(p00[q], W0, Z), seg_mul2(p01[q], W1, Z));
+        const uint64_t T1 = fadd2(seg_mul2(p10[q], W0, Z), seg_mul2(p11[q], W1, Z));
+        float va, vb;
+        f2_unpack(fadd2(seg_mul2(T0, H0[k], Z), seg_mul2(T1, H1[k], Z)), va, vb);
+        if (va == best[k]) {
+          arg[k] = 2 * q;
+          break;
+        }
+        if (vb == best[k]) {
+          arg[k] = 2 * q + 1;
+          break;
+        }
+      }
+    }  // else a tail class won outright and arg[k] is already its index
+    labels[((int64_t)b * R + oy0 + k) * R + ox] = (uint8_t)arg[k];
+  }
+}
+int launch_upsample_argmax(const float* logits, int B, int h, int C, int cp, int R, uint8_t* labels,
+                           cudaStream_t st) {
+  const size_t smem = (size_t)2 * h * ((C + 1) & ~1) * sizeof(float);
+  if (B < 1 || h < 1 || C < 1 || C > 256 || cp < C || R > 1024 || R != 14 * h || smem > 227 * 1024)
+    return VPE_E_CONFIG;
+  static bool attr = false;
+  if (!attr) {
+    VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      227 * 1024));
+    attr = true;
+  }
+  seg_upsample_argmax_kernel<<<dim3(2 * h, B), (R + 31) / 32 * 32, smem, st>>>(logits, h, C, cp, R, labels, 0.f);
+  VPE_CUDA_TRY(cudaGetLastError());
+  return VPE_OK;
 }
 }  // namespace
+
+extern "C" int vpe_op_upsample_argmax(const float* logits, int32_t B, int32_t h, int32_t C, int32_t cp,
+                                      int32_t resolution, uint8_t* labels, void* stream) {
+  if (!logits || !labels) return VPE_E_VALUE;
+  VPE_TRY(launch_upsample_argmax(logits, B, h, C, cp, resolution, labels, static_cast<cudaStream_t>(stream)));
+  count_launches(1);
+  return VPE_OK;
+}
 
 extern "C" int vpe_seg_create(const vpe_seg_config* cfg, const vpe_seg_weights* w, vpe_seg** out) {
   if (!cfg || !w || !out) return VPE_E_VALUE;
@@ -134,18 +242,7 @@ extern "C" int vpe_seg_forward(vpe_seg* s, const void* final_tap, uint8_t* label
     s->bound = final_tap;
   }
   VPE_TRY(launch_gemm(s->g, st));
-  const int R = s->cfg.resolution;
-  dim3 grid(2 * h, B);
-  const size_t smem = (size_t)2 * h * C * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      227 * 1024));
-    attr = true;
-  }
-  if (R > 1024 || R != 14 * h || smem > 227 * 1024) return VPE_E_CONFIG;
-  seg_upsample_argmax_kernel<<<grid, (R + 31) / 32 * 32, smem, st>>>(s->logits, h, C, s->cpitch, R, labels);
-  VPE_CUDA_TRY(cudaGetLastError());
+  VPE_TRY(launch_upsample_argmax(s->logits, B, h, C, s->cpitch, s->cfg.resolution, labels, st));
   count_launches(2);
   if (logits_out) {
     VPE_CUDA_TRY(cudaMemcpy2DAsync(logits_out, (size_t)C * 4, s->logits, (size_t)s->cpitch * 4, (size_t)C * 4,

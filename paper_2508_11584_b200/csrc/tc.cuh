@@ -226,12 +226,14 @@ VPE_DEV void umma_commit_pair(uint64_t* bar) {
           smem_u32(bar))
       : "memory");
 }
-// arrive on the pair leader's copy of a barrier (release at cluster scope)
+// arrive on the pair leader's copy of a barrier. Relaxed: callers order their tcgen05.ld with
+// tcgen05.wait::ld + fence::before_thread_sync; a release here compiles to MEMBAR.ALL.GPU, which
+// stalls each epilogue warp behind its own outstanding global stores.
 VPE_DEV void mbar_arrive_leader(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .b32 ra;\n\t"
       "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar))
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar))
       : "memory");
 }
 VPE_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {

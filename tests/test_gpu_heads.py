@@ -116,3 +116,30 @@ def test_det_stagewise(setup):
             assert gap <= 2 * max_err, f"top-k swap gap {gap:.3e} > 2 x max err {max_err:.3e}"
         torch.testing.assert_close(out["boxes"][b, :k].cpu(), ref[b]["boxes"], rtol=1e-5, atol=1e-3)
         torch.testing.assert_close(out["scores"][b, :k].cpu(), ref[b]["scores"], rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("B,h,C,cp", [(2, 32, 150, 160), (1, 16, 21, 32), (1, 32, 7, 8), (1, 16, 256, 256)])
+def test_upsample_argmax_exact(B, h, C, cp):
+    """The fused upsample+argmax on the SAME fp32 logits as torch's CPU F.interpolate + argmax
+    (oracle/seg.py seg_forward): labels bit-identical, including exact ties (duplicated classes,
+    a class duplicated into the tail past the last 8-class chunk, all-equal pixels, +-0)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    from paper_2508_11584_b200 import _ops
+    R = 14 * h
+    g = torch.Generator().manual_seed(7 + C)
+    lg = torch.randn(B, h * h, cp, generator=g)
+    lg[..., C:] = 1e9  # padding classes must never be read
+    if C > 8:
+        lg[..., C - 1] = lg[..., 2]            # tail class ties an early class: index 2 must win
+        lg[..., 5] = lg[..., 1]                # tie inside one chunk
+    lg[:, : h, :C] = 0.25                      # first source row: every class equal -> label 0
+    lg[:, h: 2 * h, :C] = -0.0
+    lg[:, 2 * h: 2 * h + 3, 0] = 0.0           # +0 vs -0
+    labels = _ops.upsample_argmax(lg.cuda(), h, R, classes=C)
+    torch.cuda.synchronize()
+    x = lg[..., :C].reshape(B, h, h, C).permute(0, 3, 1, 2)
+    ref = torch.nn.functional.interpolate(x, size=(R, R), mode="bilinear", align_corners=False).argmax(1)
+    ref = ref.to(torch.uint8)
+    bad = (labels.cpu() != ref).sum().item()
+    assert bad == 0, f"{bad} of {ref.numel()} labels differ"

@@ -28,9 +28,16 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--only", default="")
     p.add_argument("--conv", action="store_true")
+    p.add_argument("--bns", default="128,192,256,-128,-256")
     args = p.parse_args()
     dev = torch.device("cuda")
     res = []
+    if args.only == "seg":
+        for (B, h, C, cp) in [(16, 32, 150, 160), (1, 32, 150, 160)]:
+            lg = torch.randn(B, h * h, cp, device=dev)
+            us = timeit(lambda: _ops.upsample_argmax(lg, h, 14 * h, classes=C))
+            print(json.dumps(dict(kernel="upsample_argmax", B=B, h=h, C=C, us=us)), flush=True)
+        return
     gemms = [] if args.only == "attention" else None
     for (M, N, K) in [(16400, 1536, 384), (16400, 384, 1536), (16400, 1152, 384), (16400, 384, 384), (8192, 8192, 8192)] if gemms is None else gemms:
         a = torch.randn(M, K, device=dev).to(torch.bfloat16)
@@ -38,7 +45,7 @@ def main():
         bias = torch.zeros(N, device=dev)
         out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
         outf = torch.empty(M, N, device=dev, dtype=torch.float32)
-        for bn in (128, 192, 256):
+        for bn in [int(x) for x in args.bns.split(",")]:
             for act in (0, 1):
                 us = timeit(lambda: _ops.linear(a, w, bias=bias, out=out, act=act, bn=bn))
                 tf = 2 * M * N * K / us * 1e-6
@@ -46,6 +53,8 @@ def main():
                 print(json.dumps(res[-1]), flush=True)
         us = timeit(lambda: torch.matmul(a, w.t(), out=out))
         print(json.dumps(dict(M=M, N=N, K=K, impl="cublas", us=us, tflops=2 * M * N * K / us * 1e-6)), flush=True)
+    if args.only == "gemm":
+        return
     for (B, T, H) in [(16, 1025, 6), (1, 1025, 6), (8, 1370, 16), (1, 1370, 12)]:
         D = H * 64
         qkv = torch.randn(B * T, 3 * D, device=dev).to(torch.bfloat16)
