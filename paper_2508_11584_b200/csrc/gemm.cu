@@ -230,6 +230,90 @@ VPE_DEV void epilogue_direct(const EpiParams& ep, int64_t gpix, int col0, float 
   }
 }
 
+// EPI_CONV through a per-warp smem stage (halo conv): the warp's 32 lanes are 32 pixels of 32
+// channels at pitch ldo. Written per thread, each 16-byte store of the warp lands in a different
+// pixel (half sectors) -- measured ~1.5x slower for the whole conv than contiguous runs. So the
+// add operands are loaded and the results stored cooperatively, in passes of 8U channels:
+// piece q = 32 j + lane is 16-byte unit (q % U) of pixel q / U, i.e. each instruction moves
+// 32/U pixels x 16U contiguous bytes (U = 4: the warp's whole 2 KB when ldo = 32). Stage row of
+// pixel p: 16U bytes, units XOR-swizzled (conflict-free per pixel and per piece).
+template <int U>
+VPE_DEV uint32_t conv_stg_off(int px, int unit) {
+  constexpr int SH = U == 4 ? 1 : 2;
+  return (uint32_t)(px * 16 * U + ((unit ^ ((px >> SH) & (U - 1))) << 4));
+}
+
+template <int U>
+VPE_DEV void epilogue_conv_staged(const EpiParams& ep, int64_t gpix, bool valid, int col0, float (&v)[32],
+                                  uint8_t* stg) {
+  constexpr int PASSES = 4 / U, CH = 8 * U, PPI = 32 / U;  // channel passes, channels/pass, pixels/instr
+  const uint32_t lane = lane_id();
+  if (ep.bias) add_vec32(v, ep.bias, col0, ep.N, true);
+  int64_t pg[U];  // pixel of each piece this lane moves, and whether it exists
+  bool pv[U];
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    const int src = PPI * j + lane / U;
+    pg[j] = __shfl_sync(0xffffffffu, gpix, src);
+    pv[j] = __shfl_sync(0xffffffffu, valid ? 1 : 0, src) != 0;
+  }
+  const __nv_bfloat16* adds[2] = {ep.add1, ep.add2};
+  __nv_bfloat16* outs[2] = {reinterpret_cast<__nv_bfloat16*>(ep.out), ep.out_relu};
+#pragma unroll
+  for (int h = 0; h < PASSES; ++h) {
+    const int c = col0 + CH * h;
+    float* vh = v + CH * h;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      if (!adds[a]) continue;  // warp-uniform
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        uint4 u = make_uint4(0, 0, 0, 0);
+        if (pv[j]) u = __ldg(reinterpret_cast<const uint4*>(adds[a] + pg[j] * ep.ldo + c) + (lane % U));
+        *reinterpret_cast<uint4*>(stg + conv_stg_off<U>(PPI * j + lane / U, lane % U)) = u;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint4 w = *reinterpret_cast<const uint4*>(stg + conv_stg_off<U>(lane, u));
+        const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 f = __bfloat1622float2(hh[t]);
+          vh[8 * u + 2 * t] += f.x;
+          vh[8 * u + 2 * t + 1] += f.y;
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int j = 0; j < CH; ++j) vh[j] = apply_act(vh[j], ep.act);
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      if (!outs[o]) continue;  // warp-uniform
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float f[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) f[t] = o ? fmaxf(vh[8 * u + t], 0.f) : vh[8 * u + t];
+        uint4 w;
+        w.x = pack_bf16(f[0], f[1]);
+        w.y = pack_bf16(f[2], f[3]);
+        w.z = pack_bf16(f[4], f[5]);
+        w.w = pack_bf16(f[6], f[7]);
+        *reinterpret_cast<uint4*>(stg + conv_stg_off<U>(lane, u)) = w;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const uint4 w = *reinterpret_cast<const uint4*>(stg + conv_stg_off<U>(PPI * j + lane / U, lane % U));
+        if (pv[j]) *(reinterpret_cast<uint4*>(outs[o] + pg[j] * ep.ldo + c) + (lane % U)) = w;
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // optional MMA-thread timeline of CTA 0 (diagnostics only: VPE_GEMM_TRACE=1, vpe_debug_gemm_trace)
 __device__ unsigned long long g_gemm_trace[4096];
 static int g_gemm_trace_on = -1;
@@ -238,6 +322,17 @@ static int g_gemm_trace_on = -1;
     if (p.trace && blockIdx.x == 0 && (idx) < 2040) {                                \
       g_gemm_trace[2 * (idx)] = (unsigned long long)(code);                          \
       g_gemm_trace[2 * (idx) + 1] = (unsigned long long)clock64();                   \
+      ++(idx);                                                                       \
+    }                                                                                \
+  } while (0)
+
+// per-role variant: slots [base, base + 600) of CTA 0's timeline (halo conv: MMA 0, TMA 680,
+// epilogue warp 2 at 1360)
+#define ROLE_TRACE(base, idx, code)                                                  \
+  do {                                                                               \
+    if (p.trace && blockIdx.x == 0 && (idx) < 600) {                                 \
+      g_gemm_trace[2 * ((base) + (idx))] = (unsigned long long)(code);               \
+      g_gemm_trace[2 * ((base) + (idx)) + 1] = (unsigned long long)clock64();        \
       ++(idx);                                                                       \
     }                                                                                \
   } while (0)
@@ -324,7 +419,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPI_WARPS * 32);
+      mbar_init(&tempty[i], EPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -431,7 +526,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       if (chalf >= BN / 32) {  // narrow tile: this column slice has no chunk, release at once
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
       }
 #pragma unroll 1
       for (int c = chalf; c < BN / 32; c += EPI_SPLIT) {
@@ -441,7 +537,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tmem_ld_wait();
         if (c + EPI_SPLIT >= BN / 32) {  // this warp's last TMEM read of the tile: release it now
           tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);  // one arrival per warp (512 per-thread
+                                                      // arrivals serialise on the barrier)
         }
         const int col0 = n0 + c0;
         if (col0 >= p.ep.N) continue;  // warp-uniform
@@ -641,7 +739,13 @@ constexpr int WRES_BYTES = 72 * 1024;
 template <int BN, int KC, int RT, bool WRES = false>
 struct HaloCfg {
   static constexpr int GCH = 8 * KC;                 // channels per group
-  static constexpr int A_MAX = KC * 130 * (RT + 2) * 16;  // largest halo stage (P=130)
+  // The halo is one swizzled row of 16*KC bytes per pixel: SWIZZLE_128B for 64-channel groups,
+  // SWIZZLE_64B for 32 (TMA moves whole rows; the 16-byte rows of a no-swizzle K-major layout
+  // capped TMA at ~11 B/clk/SM, below the MMA rate). Shifted taps are plain start offsets.
+  static constexpr bool SW = true;
+  static constexpr int RB = 16 * KC;                 // bytes per halo pixel
+  static constexpr uint32_t A_LAYOUT = KC == 8 ? 2 : 4;  // UMMA SWIZZLE_128B / SWIZZLE_64B
+  static constexpr int A_MAX = (KC * 130 * (RT + 2) * 16 + 1023) / 1024 * 1024;  // largest stage (P=130)
   static constexpr int A_STAGES = 2;
   static constexpr int B_BYTES = BN * GCH * 2;       // one tap's weight tile
   static constexpr int B_STAGES = BN >= 128 ? 4 : 8;
@@ -649,7 +753,13 @@ struct HaloCfg {
   static constexpr int TMEM_COLS = GemmCfg<BN * RT, 64>::TMEM_COLS;
   static constexpr int B_SWZ = GCH == 64 ? 2 : 4;
   static constexpr int B_SBO = 8 * GCH * 2;
-  static constexpr size_t SMEM = 1024 + (size_t)A_STAGES * A_MAX + (size_t)B_REGION + 256;
+  // EPI_CONV smem stage: 16 KB, as 2 KB for each of 8 warps when a tile has <= 2 chunks per lane
+  // quadrant (whole-chunk passes, U = 4), else 1 KB for each of the 16 warps (half chunks, U = 2)
+  static constexpr int NCHUNK = RT * (BN / 32);
+  static constexpr int STG_U = NCHUNK <= 2 ? 4 : 2;
+  static constexpr int STG_SPLIT = NCHUNK <= 2 ? 2 : EPI_SPLIT;
+  static constexpr int STG_BYTES = STG_U * 512;
+  static constexpr size_t SMEM = 1024 + (size_t)A_STAGES * A_MAX + (size_t)B_REGION + 16384 + 256;
 };
 
 template <int BN, int KC, int RT, bool WRES = false>
@@ -661,7 +771,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem;  // 1024-aligned for the swizzled weight tiles
   uint8_t* sA = sB + C::B_REGION;
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(sA + C::A_STAGES * C::A_MAX);
+  uint8_t* sStg = sA + C::A_STAGES * C::A_MAX;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sStg + 16384);
   uint64_t* a_empty = a_full + C::A_STAGES;
   uint64_t* b_full = a_empty + C::A_STAGES;
   uint64_t* b_empty = b_full + C::B_STAGES;
@@ -687,7 +798,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPI_WARPS * 32);
+      mbar_init(&tempty[i], EPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -712,6 +823,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             tma_load_2d(sB + (g * nb + j) * C::B_BYTES, &tb, &b_full[0], (part * 9 + tap) * p.kcp + g * C::GCH, 0);
           }
       }
+      int tix = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
         const int img = mt / p.tiles_per_img, rr = mt - img * p.tiles_per_img;
@@ -719,8 +831,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int g = 0; g < groups; ++g, ++ia) {
           const int sa = ia % C::A_STAGES;
           mbar_wait(&a_empty[sa], ((ia / C::A_STAGES) & 1) ^ 1);
-          mbar_expect_tx(&a_full[sa], a_bytes);
-          tma_load_5d(sA + sa * C::A_MAX, &ta, &a_full[sa], 0, x0 - 1, y0 - 1, g * KC, img);
+          ROLE_TRACE(680, tix, 11);
+          if ((p.dbg & 2) && ia >= C::A_STAGES) {
+            mbar_arrive(&a_full[sa]);
+          } else {
+            mbar_expect_tx(&a_full[sa], a_bytes);
+            if (C::SW)
+              tma_load_4d(sA + sa * C::A_MAX, &ta, &a_full[sa], g * C::GCH, x0 - 1, y0 - 1, img);
+            else
+              tma_load_5d(sA + sa * C::A_MAX, &ta, &a_full[sa], 0, x0 - 1, y0 - 1, g * KC, img);
+          }
           if (WRES) continue;
           for (int j = 0; j < nb; ++j, ++ib) {
             const int sb = ib % C::B_STAGES;
@@ -736,19 +856,71 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(128, BN);
       int ia = 0, ib = 0, i = 0;
+      // descriptor words (the start-address field is the low 14 bits, in 16-byte units)
+      const uint64_t a_desc0 =
+          C::SW ? smem_desc(smem_u32(sA), 16, 8 * C::RB, C::A_LAYOUT) : smem_desc(smem_u32(sA), chunk_stride, 128, 0);
+      const uint64_t b_desc0 = smem_desc(smem_u32(sB), 16, C::B_SBO, C::B_SWZ);
+      const uint32_t a_lo0 = (uint32_t)a_desc0, a_hi = (uint32_t)(a_desc0 >> 32);
+      const uint32_t b_lo0 = (uint32_t)b_desc0, b_hi = (uint32_t)(b_desc0 >> 32);
+      const uint32_t kstep = C::SW ? 2u : (uint32_t)(2 * chunk_stride) >> 4;  // one K16 step, 16 B units
+      // SW128 starts that are not 1024-aligned (any halo pixel) need no descriptor "base offset":
+      // the swizzle is a function of the absolute smem address, which TMA and UMMA share
+      // (measured: base offset = (addr >> 7) & 7 breaks every shifted tap)
+      uint32_t toff[WRES ? 9 * RT : 1];
       if (WRES) {
+#pragma unroll
+        for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+          for (int rt = 0; rt < RT; ++rt) {
+            const uint32_t px = (uint32_t)((rt + tap / 3) * P + tap % 3);  // halo pixel of the tap
+            toff[tap * RT + rt] = C::SW ? px * (C::RB / 16) : px;
+          }
         mbar_wait(&b_full[0], 0);
         tc_fence_after();
       }
+      int tix = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
         const int acc = i & 1;
         mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+        ROLE_TRACE(0, tix, 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN * RT;
+        if (WRES) {
+          // Weights resident, so the 9 taps x RT rows x KC/2 K-steps are unrolled with every
+          // descriptor a precomputed word + constant: the lone issuing thread is latency-bound
+          // (~4 clk per dependent instruction), and at ~20 instructions per MMA it could not keep
+          // the N=32/64 MMAs (~45 clk each) fed -- the tile ran at half the tensor rate.
+          for (int g = 0; g < groups; ++g, ++ia) {
+            const int sa = ia % C::A_STAGES;
+            mbar_wait(&a_full[sa], (ia / C::A_STAGES) & 1);
+            ROLE_TRACE(0, tix, 2);
+            tc_fence_after();
+            const uint32_t a_lo = a_lo0 + (uint32_t)sa * (C::A_MAX >> 4);
+            for (int part = 0; part < p.parts; ++part) {
+              const uint32_t b_lo = b_lo0 + (uint32_t)((g * nb + part * 9) * (C::B_BYTES >> 4));
+              const uint32_t keep = (g | part) != 0 ? 1u : 0u;
+#pragma unroll
+              for (int tap = 0; tap < 9; ++tap) {
+#pragma unroll
+                for (int rt = 0; rt < RT; ++rt) {
+                  const uint32_t at = a_lo + toff[tap * RT + rt];
+#pragma unroll
+                  for (int k = 0; k < KC / 2; ++k) {
+                    const uint64_t ad = ((uint64_t)a_hi << 32) | (at + (uint32_t)k * kstep);
+                    const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + (uint32_t)(tap * (C::B_BYTES >> 4) + k * 2));
+                    umma_f16(d + rt * BN, ad, bd, idesc, (tap | k) != 0 ? 1u : keep);
+                  }
+                }
+              }
+            }
+            umma_commit(&a_empty[sa]);
+          }
+        } else {
         bool first = true;
         for (int g = 0; g < groups; ++g, ++ia) {
           const int sa = ia % C::A_STAGES;
           mbar_wait(&a_full[sa], (ia / C::A_STAGES) & 1);
+          ROLE_TRACE(0, tix, 2);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + sa * C::A_MAX);
           for (int j = 0; j < nb; ++j, ++ib) {
@@ -762,10 +934,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint32_t b0 = smem_u32(sB + (WRES ? (g * nb + j) : sb) * C::B_BYTES);
 #pragma unroll
             for (int rt = 0; rt < RT; ++rt) {
-              const uint32_t at = a0 + (uint32_t)(((rt + dy) * P + dx) * 16);
+              const uint32_t at = a0 + (uint32_t)(((rt + dy) * P + dx) * (C::SW ? C::RB : 16));
 #pragma unroll
               for (int k = 0; k < KC / 2; ++k) {
-                const uint64_t ad = smem_desc(at + 2 * k * chunk_stride, chunk_stride, 128, 0);
+                const uint64_t ad =
+                    C::SW ? smem_desc(at + 32 * k, 16, 8 * C::RB, C::A_LAYOUT)
+                          : smem_desc(at + 2 * k * chunk_stride, chunk_stride, 128, 0);
                 const uint64_t bd = smem_desc(b0 + k * 32, 16, C::B_SBO, C::B_SWZ);
                 umma_f16(d + rt * BN, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
               }
@@ -775,13 +949,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           umma_commit(&a_empty[sa]);
         }
+        }
+        ROLE_TRACE(0, tix, 3);
         umma_commit(&tfull[acc]);
       }
     }
   } else {
+    int tix = 0;
+    const bool tr = warp == 2 && lane == 0;
     const int e = warp - 2;
     const int q = warp & 3;
-    const int chalf = e >> 2;
+    // EPI_CONV goes through the per-warp smem stage (epilogue_conv_staged)
+    const bool staged =
+        p.ep.kind == EPI_CONV && (p.ep.ldo & 7) == 0 &&
+        ((reinterpret_cast<uintptr_t>(p.ep.out) | reinterpret_cast<uintptr_t>(p.ep.out_relu) |
+          reinterpret_cast<uintptr_t>(p.ep.add1) | reinterpret_cast<uintptr_t>(p.ep.add2)) & 15) == 0;
+    const int split = staged ? C::STG_SPLIT : EPI_SPLIT;
+    const int chalf = (staged && C::STG_SPLIT == 2) ? (e < 8 ? e >> 2 : 1 << 20) : e >> 2;
+    uint8_t* stg = sStg + (e & (16384 / C::STG_BYTES - 1)) * C::STG_BYTES;
     const int r = q * 32 + lane;  // virtual output position within a 128-row sub-tile
     const int ry = r / P, rx = r - (r / P) * P;
     const int rows_sub = p.bh / RT;  // output rows per 128-row sub-tile (1 when RT > 1)
@@ -792,21 +977,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int img = mt / p.tiles_per_img, rr = mt - img * p.tiles_per_img;
       const int ytile = (rr / p.tiles_x) * p.bh, x = (rr % p.tiles_x) * p.bw + rx;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
+      if (tr) ROLE_TRACE(1360, tix, 21);
       tc_fence_after();
+      if (chalf >= RT * (BN / 32)) {  // this column slice has no chunk: release at once
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
 #pragma unroll 1
-      for (int k = chalf; k < RT * (BN / 32); k += EPI_SPLIT) {
+      for (int k = chalf; k < RT * (BN / 32); k += split) {
         const int rt = k / (BN / 32), c0 = (k - rt * (BN / 32)) * 32;
         float v[32];
-        tmem_ld32(tmem + (acc * RT + rt) * BN + ((uint32_t)(q * 32) << 16) + c0, v);
-        tmem_ld_wait();
+        if (p.dbg & 32) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) v[jj] = 0.f;
+        } else {
+          tmem_ld32(tmem + (acc * RT + rt) * BN + ((uint32_t)(q * 32) << 16) + c0, v);
+          tmem_ld_wait();
+        }
+        if (k + split >= RT * (BN / 32)) {  // last TMEM read of the tile by this warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
         const int y = ytile + rt * rows_sub + ry;
         const bool valid = ry < rows_sub && rx < p.bw && y < p.H && x < p.W;
         const int64_t gpix = ((int64_t)img * p.H + y) * p.W + x;
         const int col0 = nt * BN + c0;
-        if (valid && col0 < p.ep.N) epilogue_direct(p.ep, gpix, col0, v);
+        if (staged && col0 + 32 <= p.ep.N) {
+          if (!(p.dbg & 1)) epilogue_conv_staged<C::STG_U>(p.ep, gpix, valid, col0, v, stg);
+        } else if (valid && col0 < p.ep.N && !(p.dbg & 1)) epilogue_direct(p.ep, gpix, col0, v);
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if (tr) ROLE_TRACE(1360, tix, 23);
     }
   }
   tc_fence_before();
@@ -1087,11 +1289,20 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   if ((pitch_px * 2) % 16 || (pitch_row * 2) % 16 || (pitch_img * 2) % 16 || reinterpret_cast<uintptr_t>(X) % 16)
     return VPE_E_SHAPE;
   memset(g, 0, sizeof(*g));
-  // 5D view {8 ch, x, y, chunk, img}: TMA writes [chunk][y][x][8ch] = the no-swizzle K-major layout
-  uint64_t dims[5] = {8, (uint64_t)W, (uint64_t)H, (uint64_t)(Cp / 8), (uint64_t)nimg};
-  uint64_t strides[4] = {(uint64_t)pitch_px * 2, (uint64_t)pitch_row * 2, 16, (uint64_t)pitch_img * 2};
-  uint32_t box[5] = {8u, (uint32_t)P, (uint32_t)rows_box, (uint32_t)kc, 1u};
-  VPE_TRY(encode_tma(&g->ta, 5, X, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE));
+  if (true) {
+    // 4D view {ch, x, y, img}, box {8 kc, P, rows, 1}, SWIZZLE_128B / 64B: one row per pixel
+    uint64_t dims[4] = {(uint64_t)Cp, (uint64_t)W, (uint64_t)H, (uint64_t)nimg};
+    uint64_t strides[3] = {(uint64_t)pitch_px * 2, (uint64_t)pitch_row * 2, (uint64_t)pitch_img * 2};
+    uint32_t box[4] = {8u * kc, (uint32_t)P, (uint32_t)rows_box, 1u};
+    VPE_TRY(encode_tma(&g->ta, 4, X, dims, strides, box,
+                       kc == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B));
+  } else {
+    // 5D view {8 ch, x, y, chunk, img}: TMA writes [chunk][y][x][8ch] = the no-swizzle K-major layout
+    uint64_t dims[5] = {8, (uint64_t)W, (uint64_t)H, (uint64_t)(Cp / 8), (uint64_t)nimg};
+    uint64_t strides[4] = {(uint64_t)pitch_px * 2, (uint64_t)pitch_row * 2, 16, (uint64_t)pitch_img * 2};
+    uint32_t box[5] = {8u, (uint32_t)P, (uint32_t)rows_box, (uint32_t)kc, 1u};
+    VPE_TRY(encode_tma(&g->ta, 5, X, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE));
+  }
   const int gch = 8 * kc;
   VPE_TRY(make_b_map(g, B, N, parts * 9 * Cp, ldb, bn, gch));
   g->p.mode = 2;
@@ -1127,8 +1338,16 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
 }
 
 template <int BN, int KC, int RT, bool WRES = false>
-static int launch_halo_t(const GemmPlan& g, cudaStream_t s) {
+static int launch_halo_t(const GemmPlan& g0, cudaStream_t s) {
   auto k = conv_halo_kernel<BN, KC, RT, WRES>;
+  static const int dbg = getenv("VPE_HALO_DBG") ? atoi(getenv("VPE_HALO_DBG")) : 0;
+  GemmPlan g = g0;
+  g.p.dbg = dbg;
+  if (g_gemm_trace_on < 0) {
+    const char* e = getenv("VPE_GEMM_TRACE");
+    g_gemm_trace_on = (e && e[0] == '1') ? 1 : 0;
+  }
+  g.p.trace = g_gemm_trace_on;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg<BN, KC, RT, WRES>::SMEM);

@@ -59,6 +59,7 @@ struct GemmParams {
   int hp = 0, rows_box = 0;      // halo conv: virtual row pitch P, halo rows per stage
   int parts = 1, kcp = 0;        // halo conv: split-precision weight parts, K extent per tap (Cpad)
   int trace = 0;                 // diagnostics: record the MMA timeline of CTA 0
+  int dbg = 0;                   // diagnostics (halo conv, VPE_HALO_DBG): 1 no stores, 2 no A reloads, 4 no MMA
   EpiParams ep;
 };
 

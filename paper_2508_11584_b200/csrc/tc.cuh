@@ -58,6 +58,21 @@ VPE_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Same, but the thread may stay suspended in the barrier for up to `ns` (it still resumes as soon
+// as the phase completes): for warps that wait long (epilogue on the accumulator, producer on a
+// free slot). With the default short limit they re-issue try_wait/bra ~100x per wait and steal
+// issue slots from the single MMA-issuing thread on the same SM sub-partition.
+VPE_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 1000000) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- TMA
 VPE_DEV void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");

@@ -24,6 +24,27 @@ def timeit(fn, reps=100, warm=10):
     return a.elapsed_time(b) / reps * 1e3  # us
 
 
+def timeit_graph(fn, reps=20, replays=5):
+    """Device time per call with host overhead removed: `reps` calls captured in one CUDA graph."""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(replays):
+        g.replay()
+    b.record(s)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / (reps * replays) * 1e3  # us
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--only", default="")
@@ -35,7 +56,7 @@ def main():
     if args.only == "seg":
         for (B, h, C, cp) in [(16, 32, 150, 160), (1, 32, 150, 160)]:
             lg = torch.randn(B, h * h, cp, device=dev)
-            us = timeit(lambda: _ops.upsample_argmax(lg, h, 14 * h, classes=C))
+            us = timeit_graph(lambda: _ops.upsample_argmax(lg, h, 14 * h, classes=C))
             print(json.dumps(dict(kernel="upsample_argmax", B=B, h=h, C=C, us=us)), flush=True)
         return
     gemms = [] if args.only == "attention" else None
@@ -74,7 +95,7 @@ def conv_bench():
         w = (torch.randn(N, 9 * C, device=dev) * 0.02).to(torch.bfloat16)
         bias = torch.zeros(N, device=dev)
         out = torch.empty(B, H, H, N, device=dev, dtype=torch.bfloat16)
-        us = timeit(lambda: _ops.conv(x, w, C, 3, bias=bias, out=out), reps=20, warm=3)
+        us = timeit_graph(lambda: _ops.conv(x, w, C, 3, bias=bias, out=out))
         fl = 2.0 * B * H * H * N * 9 * C
         print(json.dumps(dict(kernel="conv3x3", B=B, H=H, C=C, N=N, us=us, tflops=fl / us * 1e-6)), flush=True)
 
