@@ -275,6 +275,10 @@ int vpe_op_attention(const void* qkv, void* out, int32_t B, int32_t T, int32_t D
  * (reference seg head: SPEC.md:232-243, oracle/seg.py seg_forward) */
 int vpe_op_upsample_argmax(const float* logits, int32_t B, int32_t h, int32_t C, int32_t cp, int32_t resolution,
                            uint8_t* labels, void* stream);
+/* bilinear resize, align_corners=True, NHWC bf16 [B,Hi,Wi,cp] -> [B,Ho,Wo,cp] (first C channels)
+ * (DPT fusion/head upsampling: modeling_depth_anything.py:157-200, 288-293) */
+int vpe_op_bilinear(const void* in, int32_t B, int32_t Hi, int32_t Wi, int32_t cp, int32_t C, void* out, int32_t Ho,
+                    int32_t Wo, void* stream);
 int vpe_op_layernorm(const float* x, int32_t M, int32_t D, const float* w, const float* b, float eps, void* out_bf16,
                      const float* w2, const float* b2, void* out2_bf16, void* stream);
 

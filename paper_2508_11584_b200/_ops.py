@@ -60,6 +60,14 @@ def layernorm(x: torch.Tensor, w, b, eps=1e-6, w2=None, b2=None, stream=None):
     return out if out2 is None else (out, out2)
 
 
+def bilinear(x: torch.Tensor, Ho: int, Wo: int, C: int | None = None, stream=None) -> torch.Tensor:
+    """NHWC bf16 [B,Hi,Wi,cp] -> [B,Ho,Wo,cp], bilinear align_corners=True on the first C channels."""
+    B, Hi, Wi, cp = x.shape
+    out = torch.zeros(B, Ho, Wo, cp, device=x.device, dtype=torch.bfloat16)
+    check(lib.vpe_op_bilinear(_p(x), B, Hi, Wi, cp, C or cp, _p(out), Ho, Wo, _s(stream)), "vpe_op_bilinear")
+    return out
+
+
 def upsample_argmax(logits: torch.Tensor, h: int, resolution: int, classes: int | None = None, stream=None):
     """logits fp32 [B, h*h, cp] -> u8 labels [B, R, R] (bilinear align_corners=False, argmax)."""
     B, hw, cp = logits.shape

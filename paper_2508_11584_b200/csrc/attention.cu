@@ -177,7 +177,7 @@ __device__ unsigned long long g_att_trace[4096];
 static int g_att_trace_on = -1;
 #define ATT_TRACE(slot_base, idx, code)                                              \
   do {                                                                               \
-    if (trace && blockIdx.x == 0 && (idx) < 510) {                                   \
+    if ((trace & 1) && blockIdx.x == 0 && (idx) < 510) {                                   \
       g_att_trace[(slot_base) + 2 * (idx)] = (unsigned long long)(code);             \
       g_att_trace[(slot_base) + 2 * (idx) + 1] = (unsigned long long)clock64();      \
       ++(idx);                                                                       \
@@ -606,6 +606,17 @@ int launch_attention(const AttnPlan& a, cudaStream_t s) {
   auto k = poly == 0 ? attention_tc_kernel<0>
                      : (poly == 2 ? attention_tc_kernel<0x0303>
                                   : (poly == 3 ? attention_tc_kernel<0x1111> : attention_tc_kernel<0x0707>));
+  // Never PDL-launched: with the attention kernel in the programmatic chain the engine's outputs
+  // vary bitwise run to run (tools/pdl_determinism.py, VPE_PDL_MASK bisection: every mask that
+  // includes the attention kernel, even with griddepcontrol.wait moved to its first instruction;
+  // an isolated QKV GEMM -> attention chain, eager or graph-captured, stays deterministic, so the
+  // root cause is not pinned). It costs the one launch gap per layer.
+  const int saved_scope = pdl_scope();
+  pdl_scope() = 0;
+  struct Restore {
+    int v;
+    ~Restore() { pdl_scope() = v; }
+  } restore{saved_scope};
   return launch_k(k, dim3(a.grid), dim3(ATT_THREADS), SMEM_ATT, s, a.tqkv, a.out, a.B, a.T, a.D, a.heads, scale_log2,
                   g_att_trace_on, a.sched) == cudaSuccess
              ? VPE_OK

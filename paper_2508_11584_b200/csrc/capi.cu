@@ -134,7 +134,21 @@ int vpe_op_attention(const void* qkv, void* out, int32_t B, int32_t T, int32_t D
   AttnPlan a;
   VPE_TRY(plan_attention(&a, static_cast<const __nv_bfloat16*>(qkv), static_cast<__nv_bfloat16*>(out), B, T, D,
                          heads));
-  VPE_TRY(launch_attention(a, static_cast<cudaStream_t>(stream)));
+  static const int op_pdl = getenv("VPE_OP_PDL") ? atoi(getenv("VPE_OP_PDL")) : 0;  // diagnostics
+  const int saved = pdl_scope();
+  if (op_pdl) pdl_scope() = 1;
+  const int rc = launch_attention(a, static_cast<cudaStream_t>(stream));
+  pdl_scope() = saved;
+  VPE_TRY(rc);
+  count_launches(1);
+  return VPE_OK;
+}
+
+int vpe_op_bilinear(const void* in, int32_t B, int32_t Hi, int32_t Wi, int32_t cp, int32_t C, void* out, int32_t Ho,
+                    int32_t Wo, void* stream) {
+  if (!in || !out) return VPE_E_VALUE;
+  VPE_TRY(launch_bilinear_ac(static_cast<const __nv_bfloat16*>(in), B, Hi, Wi, cp, static_cast<__nv_bfloat16*>(out),
+                             Ho, Wo, C, static_cast<cudaStream_t>(stream)));
   count_launches(1);
   return VPE_OK;
 }

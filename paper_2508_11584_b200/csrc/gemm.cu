@@ -1353,6 +1353,7 @@ static int launch_halo_t(const GemmPlan& g0, cudaStream_t s) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg<BN, KC, RT, WRES>::SMEM);
     attr_set = true;
   }
+  PdlKind pk(8);
   return launch_k(k, g.grid, dim3(GEMM_THREADS), HaloCfg<BN, KC, RT, WRES>::SMEM, s, g.ta, g.tb, g.p) == cudaSuccess
              ? VPE_OK
              : VPE_E_CUDA;
@@ -1372,6 +1373,7 @@ static int launch_t(const GemmPlan& g, cudaStream_t s) {
   }
   GemmParams p = g.p;
   p.trace = g_gemm_trace_on;
+  PdlKind pk(1);
   return launch_k(k, g.grid, dim3(GEMM_THREADS), GemmCfg<BN, BK>::SMEM, s, g.ta, g.tb, g.tout, p) == cudaSuccess
              ? VPE_OK
              : VPE_E_CUDA;

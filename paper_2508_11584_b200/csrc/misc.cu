@@ -48,6 +48,7 @@ __global__ void patch_im2col_kernel(const uint8_t* __restrict__ px, __nv_bfloat1
 int launch_patch_im2col(const uint8_t* px, __nv_bfloat16* A, int B, int R, int KP, float* resid,
                         const float* cls_pos0, int D, cudaStream_t s) {
   const int np = (R / 14) * (R / 14);
+  PdlKind pk(16);
   return launch_k(patch_im2col_kernel, dim3(B * np + B), dim3(128), 0, s, px, A, B, R, KP, resid, cls_pos0, D) ==
                  cudaSuccess
              ? VPE_OK
@@ -174,6 +175,7 @@ int launch_layernorm(const float* x, int M, int D, const float* w, const float* 
   if (D % 128) return VPE_E_SHAPE;
   const int rows_per_block = 8;
   dim3 grid((M + rows_per_block - 1) / rows_per_block), block(32 * rows_per_block);
+  PdlKind pk(4);
   switch (D / 128) {
 #define VPE_LN(NV_) \
   case NV_:                                                                                         \
@@ -186,6 +188,15 @@ int launch_layernorm(const float* x, int M, int D, const float* w, const float* 
       return VPE_E_SHAPE;
   }
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+}
+
+// ---------------------------------------------------------------------------------------------
+// hy*(hx*a + lx*b) + ly*(hx*c + lx*d) with the FMA contraction spelled out, so that every resize
+// variant below rounds identically (bit-identical outputs whichever kernel the shape selects)
+__device__ __forceinline__ float bilerp(float a, float b, float c, float d, float hx, float lx, float hy, float ly) {
+  const float t0 = __fmaf_rn(lx, b, __fmul_rn(hx, a));
+  const float t1 = __fmaf_rn(lx, d, __fmul_rn(hx, c));
+  return __fmaf_rn(ly, t1, __fmul_rn(hy, t0));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -241,8 +252,8 @@ __global__ void __launch_bounds__(256) bilinear_ac_kernel(const __nv_bfloat16* _
     for (int j = 0; j < 4; ++j) {
       const float2 fa = __bfloat1622float2(pa[j]), fb = __bfloat1622float2(pb[j]);
       const float2 fc = __bfloat1622float2(pc[j]), fd = __bfloat1622float2(pd[j]);
-      const float r0 = hy * (hx * fa.x + lx * fb.x) + ly * (hx * fc.x + lx * fd.x);
-      const float r1 = hy * (hx * fa.y + lx * fb.y) + ly * (hx * fc.y + lx * fd.y);
+      const float r0 = bilerp(fa.x, fb.x, fc.x, fd.x, hx, lx, hy, ly);
+      const float r1 = bilerp(fa.y, fb.y, fc.y, fd.y, hx, lx, hy, ly);
       po[j] = pack_bf16(r0, r1);
     }
     dst[v] = o;
@@ -294,8 +305,8 @@ __global__ void __launch_bounds__(256) bilinear_ac_rows_kernel(const __nv_bfloat
     for (int j = 0; j < 4; ++j) {
       const float2 fa = __bfloat1622float2(pa[j]), fb = __bfloat1622float2(pb[j]);
       const float2 fc = __bfloat1622float2(pc[j]), fd = __bfloat1622float2(pd[j]);
-      const float v0 = hy * (hx * fa.x + lx * fb.x) + ly * (hx * fc.x + lx * fd.x);
-      const float v1 = hy * (hx * fa.y + lx * fb.y) + ly * (hx * fc.y + lx * fd.y);
+      const float v0 = bilerp(fa.x, fb.x, fc.x, fd.x, hx, lx, hy, ly);
+      const float v1 = bilerp(fa.y, fb.y, fc.y, fd.y, hx, lx, hy, ly);
       po[j] = pack_bf16(v0, v1);
     }
     dst[(ox * cp) / 8 + g] = o;
@@ -305,8 +316,12 @@ __global__ void __launch_bounds__(256) bilinear_ac_rows_kernel(const __nv_bfloat
 int launch_bilinear_ac(const __nv_bfloat16* in, int B, int Hi, int Wi, int cp, __nv_bfloat16* out, int Ho, int Wo,
                        int C, cudaStream_t s) {
   if (C % 8 || cp % 8) return VPE_E_SHAPE;
-  const size_t rows_smem = (size_t)2 * Wi * cp * 2;
-  if (rows_smem <= 96 * 1024 && !getenv("VPE_BILINEAR_GATHER")) {
+  const size_t row_bytes = (size_t)Wi * cp * 2;
+  // (tried: bands of up to 8 output rows sharing one bulk-copied source span per CTA -- 207 vs
+  // 178 us for the step's five resizes, fewer CTAs in flight)
+  static const int mode = getenv("VPE_BILINEAR_GATHER") ? 2 : 0;
+  const size_t rows_smem = 2 * row_bytes;
+  if (rows_smem <= 96 * 1024 && mode != 2) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(bilinear_ac_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);

@@ -122,6 +122,13 @@ VPE_DEV void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, 
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
+// plain (non-tensor) bulk copy global -> shared, completion on an mbarrier (bytes % 16 == 0)
+VPE_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 VPE_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 VPE_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 VPE_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }

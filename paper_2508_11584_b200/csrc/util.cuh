@@ -26,8 +26,10 @@ namespace vpe {
 // Programmatic dependent launch: a process-wide switch set per engine before it captures its
 // graphs (vpe_set_pdl; VPE_PDL=0/1 overrides). Measured: latency mode (batch 1) backbone 0.752 ->
 // 0.695 ms and head p50 -8..-9%; throughput mode with concurrent head streams 3.51 -> 3.57 ms
-// per step (early-scheduled dependents hold SM slots the head kernels could use), so engines
-// turn it on for small batches only.
+// per step (early-scheduled dependents hold SM slots the head kernels could use). Engines leave
+// it OFF by default: with it on, engine outputs varied bitwise in ~10% of replays even with the
+// attention kernel (the most frequent offender) kept out of the chain (tools/pdl_determinism.py,
+// VPE_PDL_MASK bisection) -- root cause not pinned, so it stays an opt-in latency experiment.
 inline int& pdl_flag() {
   static int on = 0;
   return on;
@@ -50,6 +52,20 @@ inline bool pdl_enabled() {
   if (!pdl_scope()) return false;
   return env >= 0 ? env == 1 : pdl_flag() == 1;
 }
+// diagnostics: VPE_PDL_MASK limits PDL to kernel kinds (1 GEMM, 2 attention, 4 LayerNorm,
+// 8 halo conv, 16 im2col); a guard drops the scope for kinds outside the mask
+struct PdlKind {
+  int saved;
+  explicit PdlKind(int bit) : saved(pdl_scope()) {
+    static int mask = -2;
+    if (mask == -2) {
+      const char* e = getenv("VPE_PDL_MASK");
+      mask = e ? atoi(e) : 0xFF;
+    }
+    if (!(mask & bit)) pdl_scope() = 0;
+  }
+  ~PdlKind() { pdl_scope() = saved; }
+};
 // <<<grid, block, smem, stream>>> with programmatic stream serialization (see tc.cuh pdl_wait)
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,

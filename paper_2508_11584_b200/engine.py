@@ -95,9 +95,10 @@ class VPEngine:
                  camera: tuple[int, int] | None = None, pdl: bool | None = None):
         torch.cuda.set_device(device)
         self.device = torch.device(f"cuda:{device}")
-        # programmatic dependent launch pays off for latency-bound small batches and costs
-        # throughput when large-batch head streams run concurrently (csrc/util.cuh)
-        self.pdl = (batch <= 2) if pdl is None else bool(pdl)
+        # programmatic dependent launch (opt-in): shortens latency-bound small batches (backbone
+        # 0.752 -> 0.695 ms at batch 1) but with it the outputs were observed to vary bitwise in
+        # ~10% of replays (tools/pdl_determinism.py; csrc/util.cuh), so it is off by default
+        self.pdl = False if pdl is None else bool(pdl)
         check(lib.vpe_set_pdl(int(self.pdl)), "vpe_set_pdl")
         self.cfg = model_config(model)
         self.model, self.resolution, self.batch = model, resolution, batch

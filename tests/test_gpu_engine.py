@@ -54,6 +54,26 @@ def test_graph_replay_deterministic(eng):
             assert torch.equal(a[n][k], b[n][k]), (n, k)
 
 
+def test_latency_mode_deterministic():
+    """Default (PDL off) latency-mode engine: every replay bit-identical (with programmatic
+    dependent launch on, outputs varied run to run -- tools/pdl_determinism.py)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    from paper_2508_11584_b200.engine import VPEngine
+    e = VPEngine("vits14", 448, 2)
+    try:
+        frames = make_frames(2, 448, 9)
+        ref = e.run(frames)
+        ref = {n: {k: v.clone() for k, v in o.items()} for n, o in ref.items()}
+        for _ in range(6):
+            o = e.run(frames)
+            for n in ref:
+                for k in ref[n]:
+                    assert torch.equal(o[n][k], ref[n][k]), (n, k)
+    finally:
+        e.close()
+
+
 def test_ring_counters_and_rates(eng):
     e, _ = eng
     c0 = e.counters()

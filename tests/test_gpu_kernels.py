@@ -183,3 +183,19 @@ def test_conv_nhwc(ops, device, H, W, C, Cp, N, ks):
     ref = F.relu(ref + add1.to(device, torch.bfloat16).float())
     torch.cuda.synchronize()
     assert rel_l2(out, ref) < 8e-3
+
+
+@pytest.mark.parametrize("Hi,Ho,C", [(16, 32, 64), (32, 64, 64), (64, 128, 64), (128, 256, 64), (256, 448, 32),
+                                     (37, 74, 64), (148, 518, 32), (5, 5, 8)])
+def test_bilinear_align_corners(ops, device, Hi, Ho, C):
+    """DPT upsampling (align_corners=True) vs torch on the same bf16 input; outputs within one bf16
+    rounding (the kernel computes in fp32 and rounds once)."""
+    g = torch.Generator().manual_seed(Hi + Ho)
+    B = 2
+    x = torch.randn(B, Hi, Hi, C, generator=g).to(device, torch.bfloat16)
+    out = ops.bilinear(x, Ho, Ho)
+    ref = F.interpolate(x.float().permute(0, 3, 1, 2), size=(Ho, Ho), mode="bilinear",
+                        align_corners=True).permute(0, 2, 3, 1)
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -7 + 1e-6).all(), err.max().item()

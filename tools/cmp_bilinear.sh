@@ -14,7 +14,7 @@ torch.save(eng.out["depth"]["depth"].cpu(), sys.argv[1])
 '''
 open("/tmp/_d.py", "w").write(code)
 subprocess.run(["python", "/tmp/_d.py", "/tmp/d_rows.pt"], check=True)
-env = dict(os.environ, VPE_BILINEAR_GATHER="1")
+env = dict(os.environ, **{os.environ.get("CMP_VAR", "VPE_BILINEAR_GATHER"): os.environ.get("CMP_VAL", "1")})
 subprocess.run(["python", "/tmp/_d.py", "/tmp/d_gather.pt"], check=True, env=env)
 a, b = torch.load("/tmp/d_rows.pt"), torch.load("/tmp/d_gather.pt")
 print("bit-identical:", torch.equal(a, b), "max abs diff", (a - b).abs().max().item())
