@@ -1283,7 +1283,8 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
     P = W + 2;
     rows = 128 / P;
   }
-  if (rows < 1 || (double)(rows * bw) / (128.0 * rt) < 0.7) return VPE_E_SHAPE;
+  static const double min_fill = getenv("VPE_HALO_FILL") ? atof(getenv("VPE_HALO_FILL")) : 0.7;
+  if (rows < 1 || (double)(rows * bw) / (128.0 * rt) < min_fill) return VPE_E_SHAPE;
   const int rows_box = rt > 1 ? rt + 2 : 129 / P + 3;
   if (P > 256 || rows_box > 256) return VPE_E_SHAPE;
   if ((pitch_px * 2) % 16 || (pitch_row * 2) % 16 || (pitch_img * 2) % 16 || reinterpret_cast<uintptr_t>(X) % 16)
