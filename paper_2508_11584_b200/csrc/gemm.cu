@@ -866,8 +866,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // SW128 starts that are not 1024-aligned (any halo pixel) need no descriptor "base offset":
       // the swizzle is a function of the absolute smem address, which TMA and UMMA share
       // (measured: base offset = (addr >> 7) & 7 breaks every shifted tap)
-      uint32_t toff[WRES ? 9 * RT : 1];
-      if (WRES) {
+      uint32_t toff[9 * RT];
+      {
 #pragma unroll
         for (int tap = 0; tap < 9; ++tap)
 #pragma unroll
@@ -875,6 +875,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint32_t px = (uint32_t)((rt + tap / 3) * P + tap % 3);  // halo pixel of the tap
             toff[tap * RT + rt] = C::SW ? px * (C::RB / 16) : px;
           }
+      }
+      if (WRES) {  // every weight tile, loaded once
         mbar_wait(&b_full[0], 0);
         tc_fence_after();
       }
@@ -885,70 +887,48 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         ROLE_TRACE(0, tix, 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN * RT;
-        if (WRES) {
-          // Weights resident, so the 9 taps x RT rows x KC/2 K-steps are unrolled with every
-          // descriptor a precomputed word + constant: the lone issuing thread is latency-bound
-          // (~4 clk per dependent instruction), and at ~20 instructions per MMA it could not keep
-          // the N=32/64 MMAs (~45 clk each) fed -- the tile ran at half the tensor rate.
-          for (int g = 0; g < groups; ++g, ++ia) {
-            const int sa = ia % C::A_STAGES;
-            mbar_wait(&a_full[sa], (ia / C::A_STAGES) & 1);
-            ROLE_TRACE(0, tix, 2);
-            tc_fence_after();
-            const uint32_t a_lo = a_lo0 + (uint32_t)sa * (C::A_MAX >> 4);
-            for (int part = 0; part < p.parts; ++part) {
-              const uint32_t b_lo = b_lo0 + (uint32_t)((g * nb + part * 9) * (C::B_BYTES >> 4));
-              const uint32_t keep = (g | part) != 0 ? 1u : 0u;
-#pragma unroll
-              for (int tap = 0; tap < 9; ++tap) {
-#pragma unroll
-                for (int rt = 0; rt < RT; ++rt) {
-                  const uint32_t at = a_lo + toff[tap * RT + rt];
-#pragma unroll
-                  for (int k = 0; k < KC / 2; ++k) {
-                    const uint64_t ad = ((uint64_t)a_hi << 32) | (at + (uint32_t)k * kstep);
-                    const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + (uint32_t)(tap * (C::B_BYTES >> 4) + k * 2));
-                    umma_f16(d + rt * BN, ad, bd, idesc, (tap | k) != 0 ? 1u : keep);
-                  }
-                }
-              }
-            }
-            umma_commit(&a_empty[sa]);
-          }
-        } else {
-        bool first = true;
+        // The 9 taps x RT rows x KC/2 K-steps are unrolled with every descriptor a precomputed
+        // word + constant: the lone issuing thread is latency-bound (~4 clk per dependent
+        // instruction), and at ~20 instructions per MMA it could not keep the N=32..128 MMAs
+        // (45-65 clk each) fed -- the tile ran at half the tensor rate. Streamed weights (not
+        // WRES) arrive one tap tile per ring slot.
         for (int g = 0; g < groups; ++g, ++ia) {
           const int sa = ia % C::A_STAGES;
           mbar_wait(&a_full[sa], (ia / C::A_STAGES) & 1);
           ROLE_TRACE(0, tix, 2);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + sa * C::A_MAX);
-          for (int j = 0; j < nb; ++j, ++ib) {
-            const int sb = ib % C::B_STAGES;
-            if (!WRES) {
-              mbar_wait(&b_full[sb], (ib / C::B_STAGES) & 1);
-              tc_fence_after();
-            }
-            const int tap = j % 9;
-            const int dy = tap / 3, dx = tap - (tap / 3) * 3;
-            const uint32_t b0 = smem_u32(sB + (WRES ? (g * nb + j) : sb) * C::B_BYTES);
+          const uint32_t a_lo = a_lo0 + (uint32_t)sa * (C::A_MAX >> 4);
+          for (int part = 0; part < p.parts; ++part) {
+            const uint32_t keep = (g | part) != 0 ? 1u : 0u;
 #pragma unroll
-            for (int rt = 0; rt < RT; ++rt) {
-              const uint32_t at = a0 + (uint32_t)(((rt + dy) * P + dx) * (C::SW ? C::RB : 16));
+            for (int tap = 0; tap < 9; ++tap) {
+              uint32_t b_lo;
+              int sb = 0;
+              if (WRES) {
+                b_lo = b_lo0 + (uint32_t)((g * nb + part * 9 + tap) * (C::B_BYTES >> 4));
+              } else {
+                sb = ib & (C::B_STAGES - 1);
+                mbar_wait(&b_full[sb], (ib / C::B_STAGES) & 1);
+                tc_fence_after();
+                b_lo = b_lo0 + (uint32_t)sb * (C::B_BYTES >> 4);
+              }
 #pragma unroll
-              for (int k = 0; k < KC / 2; ++k) {
-                const uint64_t ad =
-                    C::SW ? smem_desc(at + 32 * k, 16, 8 * C::RB, C::A_LAYOUT)
-                          : smem_desc(at + 2 * k * chunk_stride, chunk_stride, 128, 0);
-                const uint64_t bd = smem_desc(b0 + k * 32, 16, C::B_SBO, C::B_SWZ);
-                umma_f16(d + rt * BN, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+              for (int rt = 0; rt < RT; ++rt) {
+                const uint32_t at = a_lo + toff[tap * RT + rt];
+#pragma unroll
+                for (int k = 0; k < KC / 2; ++k) {
+                  const uint64_t ad = ((uint64_t)a_hi << 32) | (at + (uint32_t)k * kstep);
+                  const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + (uint32_t)(k * 2));
+                  umma_f16(d + rt * BN, ad, bd, idesc, (tap | k) != 0 ? 1u : keep);
+                }
+              }
+              if (!WRES) {
+                umma_commit(&b_empty[sb]);
+                ++ib;
               }
             }
-            first = false;
-            if (!WRES) umma_commit(&b_empty[sb]);
           }
           umma_commit(&a_empty[sa]);
-        }
         }
         ROLE_TRACE(0, tix, 3);
         umma_commit(&tfull[acc]);
