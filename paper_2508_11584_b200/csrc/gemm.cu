@@ -468,7 +468,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(128, BN);
-      int it = 0, i = 0, tn = 0;
+      // descriptor words of stage 0; a stage / K-step is a constant added to the address field
+      // (16-byte units): the single issuing thread is latency-bound, so keep its chain short
+      const uint64_t a_desc0 = smem_desc(smem_u32(sA), 16, C::SBO, C::SWZ_LAYOUT);
+      const uint64_t b_desc0 = smem_desc(smem_u32(sB), 16, C::SBO, C::SWZ_LAYOUT);
+      const uint32_t a_hi = (uint32_t)(a_desc0 >> 32), b_hi = (uint32_t)(b_desc0 >> 32);
+      int s = 0, i = 0, tn = 0;
+      uint32_t ph = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
         const int acc = i & 1;
         GEMM_TRACE(tn, 1);
@@ -476,21 +482,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tc_fence_after();
         GEMM_TRACE(tn, 2);
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
-          const int s = it % C::STAGES;
-          const uint32_t ph = (it / C::STAGES) & 1;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          GEMM_TRACE(tn, 10 + kb);
-          const uint32_t a0 = smem_u32(sA + s * C::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + s * C::B_BYTES);
+          const uint32_t a_lo = (uint32_t)a_desc0 + (uint32_t)s * (C::A_BYTES >> 4);
+          const uint32_t b_lo = (uint32_t)b_desc0 + (uint32_t)s * (C::B_BYTES >> 4);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = smem_desc(a0 + k * 32, 16, C::SBO, C::SWZ_LAYOUT);
-            const uint64_t bd = smem_desc(b0 + k * 32, 16, C::SBO, C::SWZ_LAYOUT);
+            const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo + 2 * k);
+            const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + 2 * k);
             umma_f16(d, ad, bd, idesc, (kb | k) != 0);
           }
           umma_commit(&empty[s]);
+          if (++s == C::STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         umma_commit(&tfull[acc]);
       }

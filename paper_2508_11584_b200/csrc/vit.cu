@@ -38,6 +38,9 @@ static constexpr int KPATCH = 640;
 // narrower tiles so the persistent grid still covers the SMs.
 static int pick_bn(int N, int M) {
   const int m_tiles = (M + 127) / 128;
+  // 256-wide tiles. (BN = 192 for the N = 384 proj / FC2 wins alone -- FC2 with the residual
+  // epilogue 25.4 -> 22.8 us, graph-timed microbench -- but made the backbone step slower,
+  // 2.15 -> 2.23 ms, in the pipelined engine; measured twice this round.)
   int bn = 256;
   while (bn > 64 && m_tiles * ((N + bn - 1) / bn) < 148) bn >>= 1;
   return bn;

@@ -68,11 +68,16 @@ def main():
         outf = torch.empty(M, N, device=dev, dtype=torch.float32)
         for bn in [int(x) for x in args.bns.split(",")]:
             for act in (0, 1):
-                us = timeit(lambda: _ops.linear(a, w, bias=bias, out=out, act=act, bn=bn))
+                us = timeit_graph(lambda: _ops.linear(a, w, bias=bias, out=out, act=act, bn=bn))
                 tf = 2 * M * N * K / us * 1e-6
                 res.append(dict(M=M, N=N, K=K, bn=bn, act=act, us=us, tflops=tf))
                 print(json.dumps(res[-1]), flush=True)
-        us = timeit(lambda: torch.matmul(a, w.t(), out=out))
+        if N == 384:  # the backbone's proj / FC2: LayerScale + fp32 residual reduce-add epilogue
+            resid = torch.zeros(M, N, device=dev)
+            for bn in [int(x) for x in args.bns.split(",")]:
+                us = timeit_graph(lambda: _ops.linear(a, w, bias=bias, scale=bias, out=resid, kind=_ops.EPI_RESID, bn=bn))
+                print(json.dumps(dict(M=M, N=N, K=K, bn=bn, kind="resid", us=us)), flush=True)
+        us = timeit_graph(lambda: torch.matmul(a, w.t(), out=out))
         print(json.dumps(dict(M=M, N=N, K=K, impl="cublas", us=us, tflops=2 * M * N * K / us * 1e-6)), flush=True)
     if args.only == "gemm":
         return
