@@ -258,6 +258,12 @@ int vpe_op_linear(const void* A, int32_t M, int32_t K, const void* W, int32_t N,
                   const float* scale, void* out, int32_t kind, int32_t act, int32_t bn, void* stream);
 /* bn > 0: one-CTA 128 x bn tiles; bn < 0: CTA-pair (cta_group::2) 256 x |bn| tiles */
 /* camera ingest alone: [B,H,W,3] u8 -> normalised bf16 patch rows [B*(R/14)^2, 640] (k = c*196+ky*14+kx) */
+/* out bf16 [M, N] = act(LayerNorm(x) W^T + bias) with the LayerNorm (x fp32 [M, D], D = 384)
+ * computed inside the GEMM; optional tap_out bf16 [M, D] = LayerNorm with (tap_w, tap_b)
+ * (DINOv2 block norm1 -> attention.qkv / norm2 -> mlp.fc1: modeling_dinov2.py:382-420) */
+int vpe_op_linear_ln(const float* x, int32_t M, int32_t D, const float* ln_w, const float* ln_b, float eps,
+                     const float* tap_w, const float* tap_b, void* tap_out, const void* W, int32_t N, const float* bias,
+                     int32_t act, void* out, void* stream);
 int vpe_op_camera_im2col(const void* frames_hwc_u8, int32_t B, int32_t height, int32_t width, int32_t resolution,
                          void* out_bf16, void* stream);
 /* 3x3 or 1x1 same-padding conv on NHWC bf16 x [B,H,W,Cp] with weights [N, ks*ks*Cp] -> out bf16 NHWC

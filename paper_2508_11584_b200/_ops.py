@@ -60,6 +60,19 @@ def layernorm(x: torch.Tensor, w, b, eps=1e-6, w2=None, b2=None, stream=None):
     return out if out2 is None else (out, out2)
 
 
+def linear_ln(x: torch.Tensor, ln_w, ln_b, eps: float, w: torch.Tensor, bias=None, act=ACT_NONE,
+              tap_w=None, tap_b=None, stream=None):
+    """act(LayerNorm(x) @ w.T + bias), LayerNorm inside the GEMM; x fp32 [M, 384]. Returns
+    (out bf16 [M, N], tap bf16 [M, 384] or None)."""
+    M, D = x.shape
+    N = w.shape[0]
+    out = torch.empty(M, N, device=x.device, dtype=torch.bfloat16)
+    tap = torch.empty(M, D, device=x.device, dtype=torch.bfloat16) if tap_w is not None else None
+    check(lib.vpe_op_linear_ln(_p(x), M, D, _p(ln_w), _p(ln_b), eps, _p(tap_w), _p(tap_b), _p(tap), _p(w), N,
+                               _p(bias), act, _p(out), _s(stream)), "vpe_op_linear_ln")
+    return out, tap
+
+
 def bilinear(x: torch.Tensor, Ho: int, Wo: int, C: int | None = None, stream=None) -> torch.Tensor:
     """NHWC bf16 [B,Hi,Wi,cp] -> [B,Ho,Wo,cp], bilinear align_corners=True on the first C channels."""
     B, Hi, Wi, cp = x.shape

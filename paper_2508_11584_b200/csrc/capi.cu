@@ -87,6 +87,23 @@ int vpe_op_linear(const void* A, int32_t M, int32_t K, const void* W, int32_t N,
   return VPE_OK;
 }
 
+int vpe_op_linear_ln(const float* x, int32_t M, int32_t D, const float* ln_w, const float* ln_b, float eps,
+                     const float* tap_w, const float* tap_b, void* tap_out, const void* W, int32_t N, const float* bias,
+                     int32_t act, void* out, void* stream) {
+  EpiParams ep;
+  ep.kind = EPI_BF16;
+  ep.act = act;
+  ep.N = N;
+  ep.bias = bias;
+  ep.out = out;
+  ep.ldo = N;
+  GemmPlan g;
+  VPE_TRY(plan_gemm_ln(&g, x, M, D, ln_w, ln_b, eps, tap_w, tap_b, static_cast<const __nv_bfloat16*>(W), N, ep, 256));
+  VPE_TRY(launch_gemm_ln(g, static_cast<__nv_bfloat16*>(tap_out), static_cast<cudaStream_t>(stream)));
+  count_launches(1);
+  return VPE_OK;
+}
+
 int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32_t Cp, int32_t ks, const void* w,
                 int32_t N, const float* bias, const void* add1, const void* add2, void* out, void* out_relu,
                 int32_t ldo, int32_t act, void* stream) {

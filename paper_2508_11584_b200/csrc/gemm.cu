@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "gemm.cuh"
+#include "ln.cuh"
 #include "tc.cuh"
 #include "util.cuh"
 
@@ -725,6 +726,228 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// GEMM whose A operand is LayerNorm(residual), built by the epilogue warps in the prologue and
+// kept resident in smem for every N tile of the CTA's 128-row block (replaces LN kernel + GEMM
+// for the backbone's LN1 -> QKV and LN2 -> FC1 at D = 384). A: 6 K-blocks of 128 x 64 bf16 in the
+// UMMA SWIZZLE_128B K-major layout, written with st.shared exactly where TMA would have put
+// them; only B streams (32 KB per K-block instead of 48). LN math: ln.cuh (bit-identical to the
+// standalone kernel). One M block per CTA at the engine's M (129 blocks), N tiles in sequence
+// with double-buffered TMEM accumulators.
+// Measured (tools/microbench.py --only ln, graph-timed, M = 16400): QKV 24.3 us vs LN 6.0 + GEMM
+// 18.7; FC1+GELU 35.8 vs 6.2 + 27.3. The prologue (25 MB of residual, ~3.8 us) cannot overlap
+// the MMAs (every row's statistics precede its first K-block) and 129 M blocks leave 19 SMs
+// idle, so the backbone keeps the separate LayerNorm; this path is parity-tested, not used.
+// ------------------------------------------------------------------------------------------
+constexpr int LN_D = 384, LN_KB = LN_D / 64;
+constexpr int LN_BST = 3;     // B stages
+constexpr int LN_STG = 2048;  // per epilogue warp: one 32 x 32 bf16 staging buffer
+
+template <int BN>
+struct GemmLnCfg {
+  static constexpr int A_BYTES = LN_KB * 16384;
+  static constexpr int B_BYTES = BN * 64 * 2;
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
+  static constexpr size_t SMEM = 1024 + A_BYTES + (size_t)LN_BST * B_BYTES + EPI_WARPS * LN_STG + 256;
+};
+
+// smem offset of bf16 columns [c, c+4) of A row r (c % 4 == 0) in the SWIZZLE_128B K-major layout
+VPE_DEV uint32_t ln_a_off(int r, int c) {
+  const int kb = c >> 6, j = (c & 63) >> 3;
+  return (uint32_t)(kb * 16384 + (r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4) + ((c >> 2) & 1) * 8);
+}
+
+// epilogue_tma_chunk for bf16 output with a single 2 KB staging buffer per warp
+VPE_DEV void epilogue_tma_chunk1(const GemmParams& p, const CUtensorMap* tout, float (&v)[32], int col0, int row0,
+                                 uint8_t* stg) {
+  const uint32_t lane = lane_id();
+  const int N = p.ep.N;
+  const bool fullc = col0 + 32 <= N;
+  if (p.ep.bias) add_vec32(v, p.ep.bias, col0, N, fullc);
+  if (p.ep.act == ACT_GELU) {
+    gelu_poly32(v);
+  } else if (p.ep.act != ACT_NONE) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], p.ep.act);
+  }
+  if (lane == 0) bulk_wait_read0();  // the previous store from this buffer has read it
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint4 u;
+    u.x = pack_bf16(v[8 * k + 0], v[8 * k + 1]);
+    u.y = pack_bf16(v[8 * k + 2], v[8 * k + 3]);
+    u.z = pack_bf16(v[8 * k + 4], v[8 * k + 5]);
+    u.w = pack_bf16(v[8 * k + 6], v[8 * k + 7]);
+    *reinterpret_cast<uint4*>(stg + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) = u;
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tout, stg, col0, row0);
+    bulk_commit();
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_ln_kernel(const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap tout,
+                   const GemmParams p) {
+  using C = GemmLnCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C::A_BYTES;
+  uint8_t* sStg = sB + LN_BST * C::B_BYTES;
+  uint64_t* b_full = reinterpret_cast<uint64_t*>(sStg + EPI_WARPS * LN_STG);
+  uint64_t* b_empty = b_full + LN_BST;
+  uint64_t* tfull = b_empty + LN_BST;  // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint64_t* a_full = tempty + 2;
+  uint64_t* a_empty = a_full + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(a_empty + 1);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tb);
+    tma_prefetch(&tout);
+    for (int i = 0; i < LN_BST; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], EPI_WARPS);
+    }
+    mbar_init(a_full, EPI_WARPS);
+    mbar_init(a_empty, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  pdl_wait();
+  pdl_trigger();
+  const int n_tiles = p.n_tiles, m_tiles = p.m_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x)
+        for (int nt = 0; nt < n_tiles; ++nt)
+          for (int kb = 0; kb < LN_KB; ++kb) {
+            mbar_wait(&b_empty[s], ph ^ 1);
+            mbar_expect_tx(&b_full[s], C::B_BYTES);
+            tma_load_2d(sB + s * C::B_BYTES, &tb, &b_full[s], kb * 64, nt * BN);
+            if (++s == LN_BST) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN);
+      const uint64_t a_desc0 = smem_desc(smem_u32(sA), 16, 1024, 2);
+      const uint64_t b_desc0 = smem_desc(smem_u32(sB), 16, 1024, 2);
+      const uint32_t a_hi = (uint32_t)(a_desc0 >> 32), b_hi = (uint32_t)(b_desc0 >> 32);
+      int s = 0, i = 0, mi = 0;
+      uint32_t ph = 0;
+      for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x, ++mi) {
+        mbar_wait(a_full, mi & 1);  // this block's LN(x) is in smem
+        tc_fence_after();
+        for (int nt = 0; nt < n_tiles; ++nt, ++i) {
+          const int acc = i & 1;
+          mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + acc * BN;
+#pragma unroll 1
+          for (int kb = 0; kb < LN_KB; ++kb) {
+            mbar_wait(&b_full[s], ph);
+            tc_fence_after();
+            const uint32_t a_lo = (uint32_t)a_desc0 + (uint32_t)kb * (16384 >> 4);
+            const uint32_t b_lo = (uint32_t)b_desc0 + (uint32_t)s * (C::B_BYTES >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma_f16(d, ((uint64_t)a_hi << 32) | (a_lo + 2 * k), ((uint64_t)b_hi << 32) | (b_lo + 2 * k), idesc,
+                       (kb | k) != 0);
+            umma_commit(&b_empty[s]);
+            if (++s == LN_BST) {
+              s = 0;
+              ph ^= 1;
+            }
+          }
+          umma_commit(&tfull[acc]);
+        }
+        umma_commit(a_empty);  // every MMA reading this block's A has completed
+      }
+    }
+  } else {
+    const int e = warp - 2;
+    const int q = warp & 3;
+    const int chalf = e >> 2;
+    uint8_t* stg = sStg + e * LN_STG;
+    int i = 0, mi = 0;
+    for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x, ++mi) {
+      // prologue: rows e, e + 16, ... of the block -> LN -> bf16 A in smem (+ the tap LN)
+      mbar_wait(a_empty, (mi & 1) ^ 1);  // the previous block's MMAs are done with A
+#pragma unroll 1
+      for (int rl = e; rl < 128; rl += EPI_WARPS) {
+        const int64_t row = (int64_t)mt * 128 + rl;
+        if (row < p.M) {
+          float4 v[LN_D / 128];
+          ln_load<LN_D / 128>(p.ln.x, row, LN_D, lane, v);
+          float mean, rstd;
+          ln_stats<LN_D / 128>(v, LN_D, p.ln.eps, mean, rstd);
+#pragma unroll
+          for (int k = 0; k < LN_D / 128; ++k) {
+            const int c = (k * 32 + lane) * 4;
+            *reinterpret_cast<uint2*>(sA + ln_a_off(rl, c)) = ln_affine4(v[k], mean, rstd, p.ln.w, p.ln.b, c);
+            if (p.ln.tap)
+              *reinterpret_cast<uint2*>(p.ln.tap + row * LN_D + c) = ln_affine4(v[k], mean, rstd, p.ln.tw, p.ln.tb, c);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < LN_D / 128; ++k)
+            *reinterpret_cast<uint2*>(sA + ln_a_off(rl, (k * 32 + lane) * 4)) = make_uint2(0u, 0u);
+        }
+      }
+      fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full);
+      for (int nt = 0; nt < n_tiles; ++nt, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tfull[acc], (i >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = chalf; c < BN / 32; c += EPI_SPLIT) {
+          float v[32];
+          tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
+          tmem_ld_wait();
+          if (c + EPI_SPLIT >= BN / 32) {  // this warp's last TMEM read of the tile
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          const int col0 = nt * BN + c * 32;
+          if (col0 >= p.ep.N) continue;  // warp-uniform
+          epilogue_tma_chunk1(p, &tout, v, col0, mt * 128 + q * 32, stg);
+        }
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // 3x3 convolution with a shared halo tile (mode 2).
 //
 // The 4D-box implicit GEMM above re-reads the input once per tap (9x the L2->SMEM traffic).
@@ -1385,7 +1608,52 @@ static int launch_pair_t(const GemmPlan& g, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
 }
 
+int plan_gemm_ln(GemmPlan* g, const float* x, int M, int D, const float* w, const float* b, float eps,
+                 const float* tw, const float* tb, const __nv_bfloat16* B, int N, const EpiParams& ep, int bn) {
+  if (D != LN_D || bn != 256 || ep.kind != EPI_BF16 || !x || !w || !b) return VPE_E_SHAPE;
+  if (reinterpret_cast<uintptr_t>(x) % 16) return VPE_E_SHAPE;
+  memset(g, 0, sizeof(*g));
+  VPE_TRY(make_b_map(g, B, N, D, D, bn, 64));
+  g->p.ep = ep;
+  g->p.M = M;
+  VPE_TRY(make_out_map(g, M));
+  if (!g->p.tma_out) return VPE_E_SHAPE;
+  g->p.kblocks = D / 64;
+  g->p.n_tiles = (N + bn - 1) / bn;
+  g->p.m_tiles = (M + 127) / 128;
+  g->p.ln.x = x;
+  g->p.ln.w = w;
+  g->p.ln.b = b;
+  g->p.ln.eps = eps;
+  g->p.ln.tw = tw;
+  g->p.ln.tb = tb;
+  g->grid = dim3(g->p.m_tiles < num_sms() ? g->p.m_tiles : num_sms(), 1, 1);
+  g->bn = bn;
+  g->bk = 64;
+  g->ln = 1;
+  g->smem = GemmLnCfg<256>::SMEM;
+  return VPE_OK;
+}
+
+int launch_gemm_ln(const GemmPlan& g0, __nv_bfloat16* tap, cudaStream_t s) {
+  if (!g0.ln || g0.bn != 256) return VPE_E_SHAPE;
+  if (tap && (!g0.p.ln.tw || !g0.p.ln.tb)) return VPE_E_VALUE;
+  GemmPlan g = g0;
+  g.p.ln.tap = tap;
+  auto k = gemm_ln_kernel<256>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GemmLnCfg<256>::SMEM);
+    attr_set = true;
+  }
+  PdlKind pk(1);
+  return launch_k(k, g.grid, dim3(GEMM_THREADS), GemmLnCfg<256>::SMEM, s, g.tb, g.tout, g.p) == cudaSuccess
+             ? VPE_OK
+             : VPE_E_CUDA;
+}
+
 int launch_gemm(const GemmPlan& g, cudaStream_t s) {
+  if (g.ln) return launch_gemm_ln(g, nullptr, s);
   if (g.pair) {
     if (g.bn == 128) return launch_pair_t<128>(g, s);
     if (g.bn == 192) return launch_pair_t<192>(g, s);

@@ -46,6 +46,17 @@ struct EpiParams {
   float* depth = nullptr;
 };
 
+// LayerNorm computed in the GEMM prologue (gemm_ln_kernel): A = LN(x) over D = K columns
+struct LnParams {
+  const float* x = nullptr;  // fp32 residual stream [M, D]
+  const float* w = nullptr;
+  const float* b = nullptr;
+  float eps = 0.f;
+  const float* tw = nullptr;  // optional second affine written to `tap` (the ring's tap LN)
+  const float* tb = nullptr;
+  __nv_bfloat16* tap = nullptr;
+};
+
 struct GemmParams {
   int kblocks = 0;     // K blocks on the B side
   int kblocks_a = 0;   // A-side K blocks before wrap-around (split-precision weights repeat A)
@@ -61,6 +72,7 @@ struct GemmParams {
   int trace = 0;                 // diagnostics: record the MMA timeline of CTA 0
   int dbg = 0;                   // diagnostics (halo conv, VPE_HALO_DBG): 1 no stores, 2 no A reloads, 4 no MMA
   EpiParams ep;
+  LnParams ln;
 };
 
 struct GemmPlan {
@@ -74,6 +86,7 @@ struct GemmPlan {
   int halo_rt = 1;
   int halo_wres = 0;  // 1: conv_halo_kernel<.., WRES> (all weight tiles resident in smem)
   int pair = 0;     // 1: gemm_pair_kernel<bn> (cta_group::2, 256-row tiles)
+  int ln = 0;       // 1: gemm_ln_kernel<bn> (A = LayerNorm(p.ln.x) built in the prologue)
   size_t smem = 0;
 };
 
@@ -98,6 +111,12 @@ int plan_gemm_conv(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
                    int64_t pitch_px, int64_t pitch_row, int64_t pitch_img, int ks, int bk,
                    const __nv_bfloat16* B, int N, int Kb, int64_t ldb, const EpiParams& ep, int bn);
 int launch_gemm(const GemmPlan& g, cudaStream_t stream);
+// A = LayerNorm(x) (x fp32 [M, D], D = 384) computed by the GEMM itself and kept resident in smem
+// for all N tiles of its 128-row block; B [N, D] K-major; EPI_BF16 output (bias, optional GELU).
+// The optional tap LN (second affine) is written to `tap` at launch (launch_gemm_ln).
+int plan_gemm_ln(GemmPlan* g, const float* x, int M, int D, const float* w, const float* b, float eps,
+                 const float* tw, const float* tb, const __nv_bfloat16* B, int N, const EpiParams& ep, int bn);
+int launch_gemm_ln(const GemmPlan& g, __nv_bfloat16* tap, cudaStream_t stream);
 
 }  // namespace vpe
 

@@ -7,6 +7,7 @@
 
 #include <cstdlib>
 
+#include "ln.cuh"
 #include "misc.cuh"
 #include "tc.cuh"
 #include "util.cuh"
@@ -126,47 +127,15 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int M, int D, cons
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)row * D);
   float4 v[NV];
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    v[i] = xr[i * 32 + lane];
-    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const float mean = s / D;
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const float a = v[i].x - mean, bb = v[i].y - mean, c = v[i].z - mean, d = v[i].w - mean;
-    q += (a * a + bb * bb) + (c * c + d * d);
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-  const float rstd = rsqrtf(q / D + eps);
+  ln_load<NV>(x, row, D, lane, v);
+  float mean, rstd;
+  ln_stats<NV>(v, D, eps, mean, rstd);
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     const int c = (i * 32 + lane) * 4;
-    const float n0 = (v[i].x - mean) * rstd, n1 = (v[i].y - mean) * rstd;
-    const float n2 = (v[i].z - mean) * rstd, n3 = (v[i].w - mean) * rstd;
-    if (out) {
-      const float4 ww = __ldg(reinterpret_cast<const float4*>(w + c));
-      const float4 bb = __ldg(reinterpret_cast<const float4*>(b + c));
-      uint2 u;
-      u.x = pack_bf16(n0 * ww.x + bb.x, n1 * ww.y + bb.y);
-      u.y = pack_bf16(n2 * ww.z + bb.z, n3 * ww.w + bb.w);
-      *reinterpret_cast<uint2*>(out + (int64_t)row * D + c) = u;
-    }
-    if (out2) {
-      const float4 ww = __ldg(reinterpret_cast<const float4*>(w2 + c));
-      const float4 bb = __ldg(reinterpret_cast<const float4*>(b2 + c));
-      uint2 u;
-      u.x = pack_bf16(n0 * ww.x + bb.x, n1 * ww.y + bb.y);
-      u.y = pack_bf16(n2 * ww.z + bb.z, n3 * ww.w + bb.w);
-      *reinterpret_cast<uint2*>(out2 + (int64_t)row * D + c) = u;
-    }
+    if (out) *reinterpret_cast<uint2*>(out + (int64_t)row * D + c) = ln_affine4(v[i], mean, rstd, w, b, c);
+    if (out2) *reinterpret_cast<uint2*>(out2 + (int64_t)row * D + c) = ln_affine4(v[i], mean, rstd, w2, b2, c);
   }
 }
 

@@ -199,3 +199,22 @@ def test_bilinear_align_corners(ops, device, Hi, Ho, C):
     torch.cuda.synchronize()
     err = (out.float() - ref).abs()
     assert (err <= ref.abs() * 2 ** -7 + 1e-6).all(), err.max().item()
+
+
+@pytest.mark.parametrize("M,N,act", [(16400, 1152, 0), (16400, 1536, 1), (1025, 1152, 0), (300, 1536, 1)])
+def test_linear_ln_fused_matches_unfused(ops, device, M, N, act):
+    """GEMM with LayerNorm(x) built in its prologue == LayerNorm kernel + GEMM, bit for bit (same
+    LN rounding in ln.cuh, same bf16 A, same MMA order); the tap LN output likewise."""
+    g = torch.Generator().manual_seed(M + N)
+    D = 384
+    x = (torch.randn(M, D, generator=g) * 3 + 0.5).to(device)
+    lw, lb = (torch.randn(D, generator=g) * 0.5 + 1).to(device), torch.randn(D, generator=g).to(device)
+    tw, tb = torch.randn(D, generator=g).to(device), torch.randn(D, generator=g).to(device)
+    w = (torch.randn(N, D, generator=g) * 0.05).to(device, torch.bfloat16)
+    bias = torch.randn(N, generator=g).to(device)
+    out, tap = ops.linear_ln(x, lw, lb, 1e-6, w, bias=bias, act=act, tap_w=tw, tap_b=tb)
+    xln, tap_ref = ops.layernorm(x, lw, lb, 1e-6, tw, tb)
+    ref = ops.linear(xln, w, bias=bias, act=act, bn=256)
+    torch.cuda.synchronize()
+    assert torch.equal(tap, tap_ref)
+    assert torch.equal(out, ref), (out.float() - ref.float()).abs().max().item()
