@@ -57,10 +57,11 @@ __global__ void transpose_heads_kernel(const float* __restrict__ cls_w, const fl
     for (int o = threadIdx.x; o < NO; o += blockDim.x) bcat[o] = o < A ? cls_b[o] : box_b[o - A];
 }
 
-// 1x1 cls (A) / bbox (4A) convs in fp32 FFMA, register-tiled SGEMM: a block computes 64 pixels
+// 1x1 cls (A) / bbox (4A) convs in fp32 FFMA, register-tiled SGEMM: a block computes 32 pixels
 // x 48 outputs (45 used); each thread 4 pixels x 3 outputs; K = D streamed through SMEM in chunks.
-constexpr int PX_PER_BLK = 64, KT = 32, SH_PITCH = 68, NO_PAD = 48;
-__global__ void __launch_bounds__(256) det_1x1_kernel(const float* __restrict__ hidden, int npix_total, int P,
+// (64-pixel blocks of 256 threads: 256 blocks for 148 SMs, 51 vs 47 us at B = 16.)
+constexpr int PX_PER_BLK = 32, KT = 32, SH_PITCH = 36, NO_PAD = 48, DET_THREADS = 128;
+__global__ void __launch_bounds__(DET_THREADS) det_1x1_kernel(const float* __restrict__ hidden, int npix_total, int P,
                                                       int D, int A, const float* __restrict__ wT,
                                                       const float* __restrict__ bcat, float* __restrict__ obj,
                                                       float* __restrict__ deltas) {
@@ -76,13 +77,13 @@ __global__ void __launch_bounds__(256) det_1x1_kernel(const float* __restrict__ 
     for (int j = 0; j < 3; ++j) acc[i][j] = 0.f;
   for (int k0 = 0; k0 < D; k0 += KT) {
 #pragma unroll
-    for (int j = 0; j < (PX_PER_BLK * KT) / 256; ++j) {
-      const int i = tid + 256 * j;
+    for (int j = 0; j < (PX_PER_BLK * KT) / DET_THREADS; ++j) {
+      const int i = tid + DET_THREADS * j;
       const int px = i / KT, kk = i - px * KT;
       const int gp = p0 + px;
       s_h[kk][px] = gp < npix_total ? hidden[(int64_t)gp * D + k0 + kk] : 0.f;
     }
-    for (int i = tid; i < KT * NO_PAD; i += 256) {
+    for (int i = tid; i < KT * NO_PAD; i += DET_THREADS) {
       const int kk = i / NO_PAD, o = i - kk * NO_PAD;
       s_w[kk][o] = o < NO ? __ldg(wT + (int64_t)(k0 + kk) * NO + o) : 0.f;
     }
@@ -460,7 +461,7 @@ extern "C" int vpe_det_forward(vpe_det* d, const void* final_tap, const vpe_det_
   }
   VPE_TRY(launch_gemm(d->g, st));
   const int npix = B * d->P;
-  det_1x1_kernel<<<(npix + PX_PER_BLK - 1) / PX_PER_BLK, 256, 0, st>>>(d->hidden, npix, d->P, D, A, d->wT, d->bcat, d->obj,
+  det_1x1_kernel<<<(npix + PX_PER_BLK - 1) / PX_PER_BLK, DET_THREADS, 0, st>>>(d->hidden, npix, d->P, D, A, d->wT, d->bcat, d->obj,
                                                          d->deltas);
   VPE_CUDA_TRY(cudaGetLastError());
   det_topk_kernel<<<B, 1024, 0, st>>>(d->obj, d->deltas, n, K, d->cfg, h, d->cbox, d->cscore, d->cidx, d->cvalid,
