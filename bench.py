@@ -208,12 +208,21 @@ def kernel_roofline(engine, args, peaks):
     s = torch.cuda.current_stream()
     for _ in range(10):
         _ops.linear(a, w, bias=bias, out=out, act=_ops.ACT_GELU, bn=BACKBONE_BN)
+    # 20 launches captured in one CUDA graph and replayed: the events then bracket back-to-back
+    # kernels (host-side planning/launch cost of the eager op is not part of the kernel's time)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(20):
+            _ops.linear(a, w, bias=bias, out=out, act=_ops.ACT_GELU, bn=BACKBONE_BN)
+    g.replay()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 200
+    replays = 10
+    reps = 20 * replays
     torch.cuda.synchronize()
     e0.record(s)
-    for _ in range(reps):
-        _ops.linear(a, w, bias=bias, out=out, act=_ops.ACT_GELU, bn=BACKBONE_BN)
+    for _ in range(replays):
+        g.replay()
     e1.record(s)
     torch.cuda.synchronize()
     dur = e0.elapsed_time(e1) / reps * 1e-3

@@ -340,25 +340,28 @@ VPE_DEV uint64_t fmul2(uint64_t a, uint64_t b) {
 }
 
 // exact-erf GELU (transformers activations.py:70-89) for a pair, MUFU-free:
-// erf(x/sqrt2) = xc * p(xc^2/16) with xc = clamp(x, -4, 4), p a degree-8 least-squares fit
-// (max |erf error| 2.9e-5 in fp32; max |GELU error| 1.9e-4 over [-10, 10], at the clamp, versus
-// bf16 output rounding of 4e-3 at 1.0). 17 f32x2-pipe instructions per pair.
+// Phi(x) = 0.5 + xc * q(xc^2) with xc = clamp(x, -4, 4), q a degree-8 least-squares fit of
+// (erf(x/sqrt2)/x)/2 (the 1/16 argument scale and the 1/2 folded into its coefficients; max |GELU
+// error| 1.9e-4 over [-10, 10], at the clamp, versus bf16 output rounding of 4e-3 at 1.0).
+// 11 f32x2-pipe instructions per pair.
+#define VPE_C2(c) f2_pack(c, c)
 VPE_DEV uint64_t gelu_poly2(uint64_t x) {
   float x0, x1;
   f2_unpack(x, x0, x1);
   const uint64_t xc = f2_pack(fminf(fmaxf(x0, -4.f), 4.f), fminf(fmaxf(x1, -4.f), 4.f));
-  const uint64_t u = fmul2(fmul2(xc, f2_pack(0.0625f, 0.0625f)), xc);
-  uint64_t p = ffma2(u, f2_pack(7.323220372e-01f, 7.323220372e-01f), f2_pack(-3.916897058e+00f, -3.916897058e+00f));
-  p = ffma2(p, u, f2_pack(9.367665291e+00f, 9.367665291e+00f));
-  p = ffma2(p, u, f2_pack(-1.341740036e+01f, -1.341740036e+01f));
-  p = ffma2(p, u, f2_pack(1.306751728e+01f, 1.306751728e+01f));
-  p = ffma2(p, u, f2_pack(-9.316836357e+00f, -9.316836357e+00f));
-  p = ffma2(p, u, f2_pack(5.061147213e+00f, 5.061147213e+00f));
-  p = ffma2(p, u, f2_pack(-2.125376940e+00f, -2.125376940e+00f));
-  p = ffma2(p, u, f2_pack(7.978495359e-01f, 7.978495359e-01f));
-  const uint64_t phi = ffma2(fmul2(xc, p), f2_pack(0.5f, 0.5f), f2_pack(0.5f, 0.5f));
+  const uint64_t v = fmul2(xc, xc);
+  uint64_t q = ffma2(v, VPE_C2(8.525350564e-11f), VPE_C2(-7.295789306e-09f));
+  q = ffma2(q, v, VPE_C2(2.791781810e-07f));
+  q = ffma2(q, v, VPE_C2(-6.397915058e-06f));
+  q = ffma2(q, v, VPE_C2(9.969724488e-05f));
+  q = ffma2(q, v, VPE_C2(-1.137309126e-03f));
+  q = ffma2(q, v, VPE_C2(9.885053150e-03f));
+  q = ffma2(q, v, VPE_C2(-6.641802937e-02f));
+  q = ffma2(q, v, VPE_C2(3.989247680e-01f));
+  const uint64_t phi = ffma2(xc, q, VPE_C2(0.5f));
   return fmul2(x, phi);
 }
+#undef VPE_C2
 
 VPE_DEV void gelu_poly32(float (&v)[32]) {
 #pragma unroll
