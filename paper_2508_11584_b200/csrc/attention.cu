@@ -597,6 +597,10 @@ int launch_attention(const AttnPlan& a, cudaStream_t s) {
     cudaFuncSetAttribute(attention_tc_kernel<0x0707>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
     cudaFuncSetAttribute(attention_tc_kernel<0x0303>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
     cudaFuncSetAttribute(attention_tc_kernel<0x1111>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
+    max_smem_carveout(attention_tc_kernel<0>);
+    max_smem_carveout(attention_tc_kernel<0x0707>);
+    max_smem_carveout(attention_tc_kernel<0x0303>);
+    max_smem_carveout(attention_tc_kernel<0x1111>);
   }
   const float scale_log2 = 0.125f * 1.4426950408889634f;
   if (g_att_trace_on < 0) {

@@ -474,6 +474,10 @@ extern "C" int vpe_det_forward(vpe_det* d, const void* final_tap, const vpe_det_
   const size_t smem = (size_t)K * NWORDS * 8;
   if (!attr) {
     cudaFuncSetAttribute(det_nms_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, KMAX * NWORDS * 8);
+    max_smem_carveout(det_nms_scan_kernel);
+    max_smem_carveout(det_1x1_kernel);
+    max_smem_carveout(det_topk_kernel);
+    max_smem_carveout(det_nms_mask_kernel);
     attr = true;
   }
   det_nms_scan_kernel<<<B, 512, smem, st>>>(d->mask, d->cvalid, d->cbox, d->cscore, d->cidx, K,

@@ -1562,6 +1562,7 @@ static int launch_halo_t(const GemmPlan& g0, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg<BN, KC, RT, WRES>::SMEM);
+    max_smem_carveout(k);
     attr_set = true;
   }
   PdlKind pk(8);
@@ -1576,6 +1577,7 @@ static int launch_t(const GemmPlan& g, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GemmCfg<BN, BK>::SMEM);
+    max_smem_carveout(k);
     attr_set = true;
   }
   if (g_gemm_trace_on < 0) {

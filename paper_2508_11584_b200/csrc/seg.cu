@@ -185,6 +185,7 @@ int launch_upsample_argmax(const float* logits, int B, int h, int C, int cp, int
   if (!attr) {
     VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       227 * 1024));
+    max_smem_carveout(seg_upsample_argmax_kernel);
     attr = true;
   }
   seg_upsample_argmax_kernel<<<dim3(2 * h, B), (R + 31) / 32 * 32, smem, st>>>(logits, h, C, cp, R, labels, 0.f);

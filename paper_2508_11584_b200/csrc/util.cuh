@@ -66,6 +66,21 @@ struct PdlKind {
   }
   ~PdlKind() { pdl_scope() = saved; }
 };
+// Shared-memory carveout: kernels that need little smem (LayerNorm, im2col) otherwise prefer a
+// large L1 split, and every switch between them and the ~200 KB tcgen05 kernels reconfigures
+// the SM's L1/smem split at the kernel boundary. VPE_CARVEOUT=0 disables (A/B experiments).
+inline bool carveout_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("VPE_CARVEOUT");
+    on = e ? (e[0] != '0') : 1;
+  }
+  return on == 1;
+}
+template <typename K>
+inline void max_smem_carveout(K kernel) {
+  if (carveout_on()) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
 // <<<grid, block, smem, stream>>> with programmatic stream serialization (see tc.cuh pdl_wait)
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,

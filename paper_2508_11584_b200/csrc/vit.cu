@@ -41,8 +41,9 @@ static int pick_bn(int N, int M) {
   // 256-wide tiles. (BN = 192 for the N = 384 proj / FC2 wins alone -- FC2 with the residual
   // epilogue 25.4 -> 22.8 us, graph-timed microbench -- but made the backbone step slower,
   // 2.15 -> 2.23 ms, in the pipelined engine; measured twice this round.)
-  int bn = 256;
-  while (bn > 64 && m_tiles * ((N + bn - 1) / bn) < 148) bn >>= 1;
+  static const int bn384 = getenv("VPE_BN384") ? atoi(getenv("VPE_BN384")) : 256;  // A/B experiments
+  int bn = N == 384 ? bn384 : 256;
+  while (bn > 64 && m_tiles * ((N + bn - 1) / bn) < 148) bn = bn == 192 ? 128 : bn >> 1;
   return bn;
 }
 
