@@ -264,6 +264,13 @@ int vpe_op_linear(const void* A, int32_t M, int32_t K, const void* W, int32_t N,
 int vpe_op_linear_ln(const float* x, int32_t M, int32_t D, const float* ln_w, const float* ln_b, float eps,
                      const float* tap_w, const float* tap_b, void* tap_out, const void* W, int32_t N, const float* bias,
                      int32_t act, void* out, void* stream);
+/* resid fp32 [M, 384] += ls * (A W^T + bias), A bf16 [M, K], W bf16 [384, K]; then xln bf16 =
+ * LayerNorm(resid) (ln_w, ln_b) and optionally tap_out = LayerNorm(resid) (tap_w, tap_b), in the
+ * same kernel (DINOv2 block: attention.output / mlp.fc2 + layer_scale + residual, then the next
+ * norm: modeling_dinov2.py:382-420) */
+int vpe_op_linear_resid_ln(const void* A, int32_t M, int32_t K, const void* W, const float* bias, const float* ls,
+                           float* resid, const float* ln_w, const float* ln_b, float eps, void* xln, const float* tap_w,
+                           const float* tap_b, void* tap_out, void* stream);
 int vpe_op_camera_im2col(const void* frames_hwc_u8, int32_t B, int32_t height, int32_t width, int32_t resolution,
                          void* out_bf16, void* stream);
 /* 3x3 or 1x1 same-padding conv on NHWC bf16 x [B,H,W,Cp] with weights [N, ks*ks*Cp] -> out bf16 NHWC

@@ -73,6 +73,17 @@ def linear_ln(x: torch.Tensor, ln_w, ln_b, eps: float, w: torch.Tensor, bias=Non
     return out, tap
 
 
+def linear_resid_ln(a: torch.Tensor, w: torch.Tensor, bias, ls, resid: torch.Tensor, ln_w, ln_b, eps: float,
+                    tap_w=None, tap_b=None, stream=None):
+    """resid += ls * (a @ w.T + bias) in place; returns (LayerNorm(resid) bf16, tap bf16 or None)."""
+    M, K = a.shape
+    xln = torch.empty(M, 384, device=a.device, dtype=torch.bfloat16)
+    tap = torch.empty(M, 384, device=a.device, dtype=torch.bfloat16) if tap_w is not None else None
+    check(lib.vpe_op_linear_resid_ln(_p(a), M, K, _p(w), _p(bias), _p(ls), _p(resid), _p(ln_w), _p(ln_b), eps, _p(xln),
+                                     _p(tap_w), _p(tap_b), _p(tap), _s(stream)), "vpe_op_linear_resid_ln")
+    return xln, tap
+
+
 def bilinear(x: torch.Tensor, Ho: int, Wo: int, C: int | None = None, stream=None) -> torch.Tensor:
     """NHWC bf16 [B,Hi,Wi,cp] -> [B,Ho,Wo,cp], bilinear align_corners=True on the first C channels."""
     B, Hi, Wi, cp = x.shape

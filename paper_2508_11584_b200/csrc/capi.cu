@@ -104,6 +104,18 @@ int vpe_op_linear_ln(const float* x, int32_t M, int32_t D, const float* ln_w, co
   return VPE_OK;
 }
 
+int vpe_op_linear_resid_ln(const void* A, int32_t M, int32_t K, const void* W, const float* bias, const float* ls,
+                           float* resid, const float* ln_w, const float* ln_b, float eps, void* xln, const float* tap_w,
+                           const float* tap_b, void* tap_out, void* stream) {
+  GemmPlan g;
+  VPE_TRY(plan_gemm_resid_ln(&g, static_cast<const __nv_bfloat16*>(A), M, K, static_cast<const __nv_bfloat16*>(W), bias,
+                             ls, resid, ln_w, ln_b, eps, static_cast<__nv_bfloat16*>(xln), tap_w, tap_b));
+  VPE_TRY(launch_gemm_resid_ln(g, static_cast<__nv_bfloat16*>(xln), static_cast<__nv_bfloat16*>(tap_out),
+                               static_cast<cudaStream_t>(stream)));
+  count_launches(1);
+  return VPE_OK;
+}
+
 int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32_t Cp, int32_t ks, const void* w,
                 int32_t N, const float* bias, const void* add1, const void* add2, void* out, void* out_relu,
                 int32_t ldo, int32_t act, void* stream) {

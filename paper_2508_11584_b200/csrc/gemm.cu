@@ -948,6 +948,257 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// Residual GEMM with the next LayerNorm in its epilogue (backbone proj / FC2 at D = 384):
+//   resid += LayerScale * (A W^T + bias);  xln = LN(resid) (bf16, the next GEMM's A);
+//   optionally tap = LN'(resid) with a second affine (the ring's tap / final norm).
+// A CTA owns whole 384-wide rows (one 128 x 384 accumulator: an N=256 and an N=128 MMA per K
+// step), so the row statistics never leave the CTA. Epilogue: 8 warps, two per TMEM lane
+// quadrant (192 columns each). The drained pipeline stages become the epilogue's staging: the old
+// residual arrives by TMA, the new one leaves by TMA, row sums are exchanged between the two
+// warps of a quadrant through smem + a named barrier. Replaces TMA reduce-add epilogue + the
+// standalone LayerNorm kernel; the new residual is bit-identical (same single fp32 add), the LN
+// differs from layernorm_kernel only in summation order.
+// ------------------------------------------------------------------------------------------
+constexpr int RL_N = 384, RL_ST = 3;
+constexpr int RL_SPLIT = 4;                          // epilogue warps per TMEM lane quadrant
+constexpr int RL_EW = 4 * RL_SPLIT;                  // epilogue warps
+constexpr int RL_CH = RL_N / 32 / RL_SPLIT;          // 32-column chunks per epilogue warp
+constexpr int RL_THREADS = 32 * (2 + RL_EW);         // warps: 0 TMA, 1 MMA, then the epilogue
+struct RlCfg {
+  static constexpr int A_BYTES = 128 * 64 * 2;
+  static constexpr int B_BYTES = RL_N * 64 * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;  // 64 KB; the 3 stages double as epilogue staging
+  static constexpr size_t SMEM = 1024 + (size_t)RL_ST * STAGE + 2 * RL_SPLIT * 128 * 4 + 256;
+};
+
+__global__ void __launch_bounds__(RL_THREADS, 1)
+    gemm_resid_ln_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                         const __grid_constant__ CUtensorMap tres, const __grid_constant__ CUtensorMap txln,
+                         const __grid_constant__ CUtensorMap ttap, const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* xs = reinterpret_cast<float*>(smem + RL_ST * RlCfg::STAGE);  // [2 uses][RL_SPLIT parts][128 rows]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RL_ST * RlCfg::STAGE + 2 * RL_SPLIT * 128 * 4);
+  uint64_t* empty = full + RL_ST;
+  uint64_t* tfull = empty + RL_ST;
+  uint64_t* tempty = tfull + 1;
+  uint64_t* epi_done = tempty + 1;
+  uint64_t* ebar = epi_done + 1;  // [RL_EW] per epilogue warp: old-residual TMA loads
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(ebar + RL_EW);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&ta);
+    tma_prefetch(&tb);
+    tma_prefetch(&tres);
+    tma_prefetch(&txln);
+    for (int i = 0; i < RL_ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, RL_EW);
+    mbar_init(epi_done, RL_EW);
+    for (int i = 0; i < RL_EW; ++i) mbar_init(&ebar[i], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  pdl_wait();
+  pdl_trigger();
+  const int m_tiles = p.m_tiles, kblocks = p.kblocks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0, i = 0;
+      uint32_t ph = 0;
+      for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x, ++i) {
+        // the stages double as the previous tile's epilogue staging
+        if (i > 0) mbar_wait(epi_done, (i - 1) & 1);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], RlCfg::STAGE);
+          uint8_t* st = smem + s * RlCfg::STAGE;
+          tma_load_2d(st, &ta, &full[s], kb * 64, mt * 128);
+          for (int nb = 0; nb < 3; ++nb)
+            tma_load_2d(st + RlCfg::A_BYTES + nb * 16384, &tb, &full[s], kb * 64, nb * 128);
+          if (++s == RL_ST) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id256 = idesc_bf16(128, 256), id128 = idesc_bf16(128, 128);
+      const uint64_t d0 = smem_desc(smem_u32(smem), 16, 1024, 2);
+      const uint32_t lo0 = (uint32_t)d0, hi = (uint32_t)(d0 >> 32);
+      int s = 0, i = 0;
+      uint32_t ph = 0;
+      for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x, ++i) {
+        mbar_wait(tempty, (i & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_lo = lo0 + (uint32_t)s * (RlCfg::STAGE >> 4);
+          const uint32_t b_lo = a_lo + (RlCfg::A_BYTES >> 4);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = ((uint64_t)hi << 32) | (a_lo + 2 * k);
+            umma_f16(tmem, ad, ((uint64_t)hi << 32) | (b_lo + 2 * k), id256, (kb | k) != 0);
+            umma_f16(tmem + 256, ad, ((uint64_t)hi << 32) | (b_lo + (32768 >> 4) + 2 * k), id128, (kb | k) != 0);
+          }
+          umma_commit(&empty[s]);
+          if (++s == RL_ST) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        umma_commit(tfull);
+      }
+    }
+  } else {
+    const int e = warp - 2, q = warp & 3, h = e >> 2;  // h: this warp's column part of the row
+    const int r = q * 32 + lane;                        // row of the tile
+    uint8_t* stg = smem + e * (RL_CH * 4096);           // RL_CH chunks of 32 x 32 fp32
+    const int bar_id = 1 + q;                           // the quadrant's RL_SPLIT warps
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(32 * RL_SPLIT) : "memory"); };
+    int i = 0;
+    for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x, ++i) {
+      const int row0 = mt * 128 + q * 32;
+      mbar_wait(tfull, i & 1);  // mainloop done: every stage is free for staging
+      tc_fence_after();
+      if (lane == 0) {
+        mbar_expect_tx(&ebar[e], RL_CH * 4096);
+        for (int c = 0; c < RL_CH; ++c) tma_load_2d(stg + c * 4096, &tres, &ebar[e], (h * RL_CH + c) * 32, row0);
+      }
+      mbar_wait(&ebar[e], i & 1);
+      float sum = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < RL_CH; ++c) {
+        const int col0 = (h * RL_CH + c) * 32;
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + col0, v);
+        tmem_ld_wait();
+        add_vec32(v, p.ep.bias, col0, RL_N, true);
+        mul_vec32(v, p.ep.scale, col0, RL_N, true);
+        uint8_t* cb = stg + c * 4096 + lane * 128;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          float4* sp = reinterpret_cast<float4*>(cb + ((k ^ (lane & 7)) << 4));
+          float4 o = *sp;
+          o.x = __fadd_rn(o.x, v[4 * k]);
+          o.y = __fadd_rn(o.y, v[4 * k + 1]);
+          o.z = __fadd_rn(o.z, v[4 * k + 2]);
+          o.w = __fadd_rn(o.w, v[4 * k + 3]);
+          *sp = o;
+          sum = __fadd_rn(sum, __fadd_rn(__fadd_rn(o.x, o.y), __fadd_rn(o.z, o.w)));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);  // accumulator read out
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        for (int c = 0; c < RL_CH; ++c) tma_store_2d(&tres, stg + c * 4096, (h * RL_CH + c) * 32, row0);
+        bulk_commit();
+      }
+      // row statistics: the RL_SPLIT column parts of the row meet in smem (fixed order)
+      xs[h * 128 + r] = sum;
+      pair_sync();
+      float tot = xs[r];
+#pragma unroll
+      for (int j = 1; j < RL_SPLIT; ++j) tot = __fadd_rn(tot, xs[j * 128 + r]);
+      const float mean = __fdiv_rn(tot, (float)RL_N);
+      float sq = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < RL_CH; ++c) {
+        const uint8_t* cb = stg + c * 4096 + lane * 128;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 o = *reinterpret_cast<const float4*>(cb + ((k ^ (lane & 7)) << 4));
+          const float a = __fsub_rn(o.x, mean), b = __fsub_rn(o.y, mean);
+          const float cc = __fsub_rn(o.z, mean), d = __fsub_rn(o.w, mean);
+          sq = __fadd_rn(sq, __fadd_rn(__fmaf_rn(a, a, __fmul_rn(b, b)), __fmaf_rn(cc, cc, __fmul_rn(d, d))));
+        }
+      }
+      xs[RL_SPLIT * 128 + h * 128 + r] = sq;
+      pair_sync();
+      float tq = xs[RL_SPLIT * 128 + r];
+#pragma unroll
+      for (int j = 1; j < RL_SPLIT; ++j) tq = __fadd_rn(tq, xs[RL_SPLIT * 128 + j * 128 + r]);
+      const float rstd = rsqrtf(__fadd_rn(__fdiv_rn(tq, (float)RL_N), p.ln.eps));
+      if (lane == 0) bulk_wait_read0();  // the new-residual stores have read the staging
+      __syncwarp();
+      const bool tap = p.ln.tap != nullptr;
+#pragma unroll 1
+      for (int c = 0; c < RL_CH; ++c) {
+        const int col0 = (h * RL_CH + c) * 32;
+        uint8_t* cb = stg + c * 4096;
+        float x[32];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 o = *reinterpret_cast<const float4*>(cb + lane * 128 + ((k ^ (lane & 7)) << 4));
+          x[4 * k] = o.x;
+          x[4 * k + 1] = o.y;
+          x[4 * k + 2] = o.z;
+          x[4 * k + 3] = o.w;
+        }
+        __syncwarp();  // the bf16 rows below overwrite fp32 rows other lanes read above
+        for (int o = 0; o < 2; ++o) {
+          const float* w = o ? p.ln.tw : p.ln.w;
+          const float* b = o ? p.ln.tb : p.ln.b;
+          if (!w) continue;  // uniform: no second affine
+          uint8_t* ob = cb + o * 2048 + lane * 64;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + col0 + 8 * k));
+            const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + col0 + 8 * k + 4));
+            const float4 b0 = __ldg(reinterpret_cast<const float4*>(b + col0 + 8 * k));
+            const float4 b1 = __ldg(reinterpret_cast<const float4*>(b + col0 + 8 * k + 4));
+            const float* xx = x + 8 * k;
+            uint4 u;
+            u.x = pack_bf16(__fmaf_rn(__fmul_rn(__fsub_rn(xx[0], mean), rstd), w0.x, b0.x),
+                            __fmaf_rn(__fmul_rn(__fsub_rn(xx[1], mean), rstd), w0.y, b0.y));
+            u.y = pack_bf16(__fmaf_rn(__fmul_rn(__fsub_rn(xx[2], mean), rstd), w0.z, b0.z),
+                            __fmaf_rn(__fmul_rn(__fsub_rn(xx[3], mean), rstd), w0.w, b0.w));
+            u.z = pack_bf16(__fmaf_rn(__fmul_rn(__fsub_rn(xx[4], mean), rstd), w1.x, b1.x),
+                            __fmaf_rn(__fmul_rn(__fsub_rn(xx[5], mean), rstd), w1.y, b1.y));
+            u.w = pack_bf16(__fmaf_rn(__fmul_rn(__fsub_rn(xx[6], mean), rstd), w1.z, b1.z),
+                            __fmaf_rn(__fmul_rn(__fsub_rn(xx[7], mean), rstd), w1.w, b1.w));
+            *reinterpret_cast<uint4*>(ob + ((k ^ ((lane >> 1) & 3)) << 4)) = u;
+          }
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        for (int c = 0; c < RL_CH; ++c) {
+          if (p.ln.w) tma_store_2d(&txln, stg + c * 4096, (h * RL_CH + c) * 32, row0);
+          if (tap) tma_store_2d(&ttap, stg + c * 4096 + 2048, (h * RL_CH + c) * 32, row0);
+        }
+        bulk_commit();
+        bulk_wait_read0();  // staging free for the next tile's loads
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(epi_done);
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // 3x3 convolution with a shared halo tile (mode 2).
 //
 // The 4D-box implicit GEMM above re-reads the input once per tap (9x the L2->SMEM traffic).
@@ -1654,7 +1905,83 @@ int launch_gemm_ln(const GemmPlan& g0, __nv_bfloat16* tap, cudaStream_t s) {
              : VPE_E_CUDA;
 }
 
+static int bf16_rows_map(CUtensorMap* m, const __nv_bfloat16* base, int M, int N) {
+  if (reinterpret_cast<uintptr_t>(base) % 16) return VPE_E_SHAPE;
+  uint64_t dims[2] = {(uint64_t)N, (uint64_t)M};
+  uint64_t strides[1] = {(uint64_t)N * 2};
+  uint32_t box[2] = {32u, 32u};
+  return encode_tma_t(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+int plan_gemm_resid_ln(GemmPlan* g, const __nv_bfloat16* A, int M, int K, const __nv_bfloat16* W, const float* bias,
+                       const float* ls, float* resid, const float* ln_w, const float* ln_b, float eps,
+                       __nv_bfloat16* xln, const float* tw, const float* tb) {
+  if (K % 64 || !bias || !ls || !resid || !ln_w || !ln_b) return VPE_E_SHAPE;
+  if (reinterpret_cast<uintptr_t>(A) % 16 || reinterpret_cast<uintptr_t>(resid) % 16) return VPE_E_SHAPE;
+  memset(g, 0, sizeof(*g));
+  uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
+  uint64_t strides[1] = {(uint64_t)K * 2};
+  uint32_t box[2] = {64u, 128u};
+  VPE_TRY(encode_tma(&g->ta, 2, A, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B));
+  VPE_TRY(make_b_map(g, W, RL_N, K, K, 128, 64));
+  {
+    uint64_t rd[2] = {(uint64_t)RL_N, (uint64_t)M};
+    uint64_t rs[1] = {(uint64_t)RL_N * 4};
+    uint32_t rb[2] = {32u, 32u};
+    VPE_TRY(encode_tma_t(&g->tout, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, resid, rd, rs, rb, CU_TENSOR_MAP_SWIZZLE_128B));
+  }
+  if (xln) VPE_TRY(bf16_rows_map(&g->tx, xln, M, RL_N));
+  g->p.ep.kind = EPI_RESID;
+  g->p.ep.N = RL_N;
+  g->p.ep.bias = bias;
+  g->p.ep.scale = ls;
+  g->p.ep.resid = resid;
+  g->p.ep.ldr = RL_N;
+  g->p.ep.out = xln;
+  g->p.M = M;
+  g->p.kblocks = K / 64;
+  g->p.m_tiles = (M + 127) / 128;
+  g->p.ln.w = ln_w;
+  g->p.ln.b = ln_b;
+  g->p.ln.eps = eps;
+  g->p.ln.tw = tw;
+  g->p.ln.tb = tb;
+  g->grid = dim3(g->p.m_tiles < num_sms() ? g->p.m_tiles : num_sms(), 1, 1);
+  g->resid_ln = 1;
+  g->smem = RlCfg::SMEM;
+  return VPE_OK;
+}
+
+int launch_gemm_resid_ln(const GemmPlan& g0, __nv_bfloat16* xln, __nv_bfloat16* tap, cudaStream_t s) {
+  if (!g0.resid_ln) return VPE_E_SHAPE;
+  GemmPlan g = g0;
+  if (xln && xln != g0.p.ep.out) {
+    VPE_TRY(bf16_rows_map(&g.tx, xln, g.p.M, RL_N));
+    g.p.ep.out = xln;
+  }
+  if (!g.p.ep.out) g.p.ln.w = nullptr;  // no LayerNorm output wanted (tap only)
+  CUtensorMap ttap;
+  memset(&ttap, 0, sizeof(ttap));
+  g.p.ln.tap = tap;
+  if (tap) {
+    if (!g.p.ln.tw || !g.p.ln.tb) return VPE_E_VALUE;
+    VPE_TRY(bf16_rows_map(&ttap, tap, g.p.M, RL_N));
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_resid_ln_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RlCfg::SMEM);
+    max_smem_carveout(gemm_resid_ln_kernel);
+    attr_set = true;
+  }
+  PdlKind pk(1);
+  return launch_k(gemm_resid_ln_kernel, g.grid, dim3(RL_THREADS), RlCfg::SMEM, s, g.ta, g.tb, g.tout, g.tx, ttap,
+                  g.p) == cudaSuccess
+             ? VPE_OK
+             : VPE_E_CUDA;
+}
+
 int launch_gemm(const GemmPlan& g, cudaStream_t s) {
+  if (g.resid_ln) return launch_gemm_resid_ln(g, nullptr, nullptr, s);
   if (g.ln) return launch_gemm_ln(g, nullptr, s);
   if (g.pair) {
     if (g.bn == 128) return launch_pair_t<128>(g, s);

@@ -87,6 +87,8 @@ struct GemmPlan {
   int halo_wres = 0;  // 1: conv_halo_kernel<.., WRES> (all weight tiles resident in smem)
   int pair = 0;     // 1: gemm_pair_kernel<bn> (cta_group::2, 256-row tiles)
   int ln = 0;       // 1: gemm_ln_kernel<bn> (A = LayerNorm(p.ln.x) built in the prologue)
+  int resid_ln = 0; // 1: gemm_resid_ln_kernel (residual GEMM + the next LayerNorm in the epilogue)
+  CUtensorMap tx;   // resid_ln: bf16 LayerNorm output map
   size_t smem = 0;
 };
 
@@ -117,6 +119,13 @@ int launch_gemm(const GemmPlan& g, cudaStream_t stream);
 int plan_gemm_ln(GemmPlan* g, const float* x, int M, int D, const float* w, const float* b, float eps,
                  const float* tw, const float* tb, const __nv_bfloat16* B, int N, const EpiParams& ep, int bn);
 int launch_gemm_ln(const GemmPlan& g, __nv_bfloat16* tap, cudaStream_t stream);
+// resid [M, 384] fp32 += ls * (A W^T + bias) (A bf16 [M, K], W [384, K]); then xln = LN(resid)
+// with (ln_w, ln_b) in bf16 and optionally tap = LN(resid) with (tw, tb). xln / tap pointers may
+// be given at launch (ring slots); a null xln at plan and launch skips that output.
+int plan_gemm_resid_ln(GemmPlan* g, const __nv_bfloat16* A, int M, int K, const __nv_bfloat16* W, const float* bias,
+                       const float* ls, float* resid, const float* ln_w, const float* ln_b, float eps,
+                       __nv_bfloat16* xln, const float* tw, const float* tb);
+int launch_gemm_resid_ln(const GemmPlan& g, __nv_bfloat16* xln, __nv_bfloat16* tap, cudaStream_t stream);
 
 }  // namespace vpe
 

@@ -29,6 +29,10 @@ struct vpe_vit {
   AttnPlan attn;
   MlpPlan mlp[VPE_MAX_LAYERS];
   bool fused_mlp = false;  // FC1 + GELU + FC2 + LayerScale residual in one kernel (mlp.cu)
+  // proj / FC2 with the following LayerNorm in their epilogue (gemm_resid_ln_kernel): D = 384 at
+  // large M only (the kernel owns whole rows: one CTA per 128-row block)
+  GemmPlan proj_rl[VPE_MAX_LAYERS], fc2_rl[VPE_MAX_LAYERS];
+  bool resid_ln = false;
 };
 
 static constexpr int KPATCH = 640;
@@ -128,6 +132,24 @@ extern "C" int vpe_vit_create(const vpe_vit_config* cfg, const vpe_vit_weights* 
   }
   if ((rc = plan_attention(&v->attn, v->qkv, v->ctx, B, v->T, D, cfg->heads))) return fail(rc);
   {
+    // Measured (tools/microbench.py --only rln, M = 16400): proj + LN2 20.0 -> 18.9 us, FC2 + LN1
+    // 32.9 -> 29.5 us. VPE_RESID_LN=0 keeps the separate LayerNorm kernels.
+    const char* e = getenv("VPE_RESID_LN");
+    v->resid_ln = D == 384 && (M + 127) / 128 >= 100 && !(e && e[0] == '0');
+    for (int l = 0; v->resid_ln && l < L; ++l) {
+      if ((rc = plan_gemm_resid_ln(&v->proj_rl[l], v->ctx, M, D, static_cast<const __nv_bfloat16*>(w->proj_w[l]),
+                                   w->proj_b[l], w->ls1[l], v->resid, w->ln2_w[l], w->ln2_b[l], cfg->ln_eps, v->xln,
+                                   nullptr, nullptr)))
+        return fail(rc);
+      const bool last = l + 1 == L;
+      if ((rc = plan_gemm_resid_ln(&v->fc2_rl[l], v->hid, M, Hd, static_cast<const __nv_bfloat16*>(w->fc2_w[l]),
+                                   w->fc2_b[l], w->ls2[l], v->resid, last ? w->norm_w : w->ln1_w[l + 1],
+                                   last ? w->norm_b : w->ln1_b[l + 1], cfg->ln_eps, last ? nullptr : v->xln,
+                                   last ? nullptr : w->norm_w, last ? nullptr : w->norm_b)))
+        return fail(rc);
+    }
+  }
+  {
     // Opt-in (VPE_FUSED_MLP=1): correct (tests/test_gpu_kernels.py::test_fused_mlp) but measured
     // slower than the FC1 / FC2 pair at C2 (70.9 vs 52 us per layer): with the 96 KB X block
     // resident, the W1 ring only holds 8 KB k-blocks of N = 64 MMAs, and per-k-block barrier
@@ -176,6 +198,25 @@ static int vit_blocks_impl(vpe_vit* v, void* const* taps, cudaStream_t s) {
   VPE_TRY(launch_gemm(v->patch, s));
   count_launches(1);
   int tap = 0;
+  if (v->resid_ln) {
+    __nv_bfloat16* t0 = (c.taps[0] == 0) ? static_cast<__nv_bfloat16*>(taps[tap++]) : nullptr;
+    VPE_TRY(launch_layernorm(v->resid, M, D, w.ln1_w[0], w.ln1_b[0], c.ln_eps, v->xln, w.norm_w, w.norm_b, t0, s));
+    for (int l = 0; l < c.depth; ++l) {
+      VPE_TRY(launch_gemm(v->qkv_g[l], s));
+      VPE_TRY(launch_attention(v->attn, s));
+      VPE_TRY(launch_gemm_resid_ln(v->proj_rl[l], nullptr, nullptr, s));
+      VPE_TRY(launch_gemm(v->fc1_g[l], s));
+      if (l + 1 < c.depth) {
+        __nv_bfloat16* t = (tap < 3 && c.taps[tap] == l + 1) ? static_cast<__nv_bfloat16*>(taps[tap++]) : nullptr;
+        VPE_TRY(launch_gemm_resid_ln(v->fc2_rl[l], nullptr, t, s));
+      } else {
+        VPE_TRY(launch_gemm_resid_ln(v->fc2_rl[l], static_cast<__nv_bfloat16*>(taps[3]), nullptr, s));
+      }
+      count_launches(5);
+    }
+    count_launches(1);
+    return VPE_OK;
+  }
   for (int l = 0; l < c.depth; ++l) {
     // LN1 of block l; if block l-1 was a tap, the same pass writes the tap LN into the ring slot
     __nv_bfloat16* tap_out = nullptr;

@@ -34,3 +34,37 @@ def test_backbone_taps_vs_oracle(device, R, B):
     for k, (g, r) in enumerate(zip(taps, ref)):
         e, c = rel_l2(g.cpu(), r), cosine(g.cpu(), r)
         assert e <= 1e-2 and c >= 0.999, f"tap {k}: rel-L2 {e:.3e} cos {c:.6f}"
+
+
+def test_backbone_batch16_fused_resid_ln(device, monkeypatch):
+    """At batch 16 (448) the proj / FC2 GEMMs carry the following LayerNorm in their epilogue
+    (gemm_resid_ln_kernel). Frame 0's taps vs the fp32 oracle at the north-star bar, and all 16
+    frames vs the unfused path (VPE_RESID_LN=0: TMA reduce-add GEMMs + layernorm_kernel)."""
+    from paper_2508_11584_b200.backbone import Backbone
+    R, B = 448, 16
+    cfg = model_config("vits14")
+    W = make_weights("vits14", heads=())
+    frames = make_frames(B, R, 4)
+    T = tokens(R)
+
+    def run():
+        bb = Backbone(W, cfg.backbone, R, B, device)
+        taps = [torch.empty(B, T, cfg.backbone.dim, device=device, dtype=torch.bfloat16) for _ in range(4)]
+        bb.forward(frames.to(device), taps)
+        torch.cuda.synchronize()
+        bb.close()
+        return [t.cpu() for t in taps]
+
+    monkeypatch.delenv("VPE_RESID_LN", raising=False)
+    fused = run()
+    monkeypatch.setenv("VPE_RESID_LN", "0")
+    plain = run()
+    ref = ovit.backbone_forward(frames[:1], W, cfg.backbone.depth, cfg.backbone.heads, cfg.backbone.taps)
+    for k in range(4):
+        e, c = rel_l2(fused[k][:1], ref[k]), cosine(fused[k][:1], ref[k])
+        assert e <= 1e-2 and c >= 0.999, f"tap {k} vs oracle: rel-L2 {e:.3e} cos {c:.6f}"
+        e2 = rel_l2(fused[k], plain[k])
+        assert e2 <= 5e-3, f"tap {k} fused vs unfused: rel-L2 {e2:.3e}"
+    # the two paths round LayerNorm sums differently, so identical taps would mean the fused
+    # kernel never ran
+    assert any(not torch.equal(f, p) for f, p in zip(fused, plain))

@@ -218,3 +218,31 @@ def test_linear_ln_fused_matches_unfused(ops, device, M, N, act):
     torch.cuda.synchronize()
     assert torch.equal(tap, tap_ref)
     assert torch.equal(out, ref), (out.float() - ref.float()).abs().max().item()
+
+
+@pytest.mark.parametrize("M,K,tap", [(16400, 384, False), (16400, 1536, True), (1025, 384, True), (300, 1536, False)])
+def test_linear_resid_ln(ops, device, M, K, tap):
+    """Residual GEMM with the next LayerNorm in its epilogue vs the unfused pair (TMA reduce-add
+    GEMM, then layernorm_kernel): the new residual bit-identical; LN outputs within one bf16 ulp
+    (only the row-sum order differs)."""
+    g = torch.Generator().manual_seed(M + K)
+    D = 384
+    a = torch.randn(M, K, generator=g).to(device, torch.bfloat16)
+    w = (torch.randn(D, K, generator=g) * 0.05).to(device, torch.bfloat16)
+    bias, ls = torch.randn(D, generator=g).to(device), (torch.rand(D, generator=g) + 0.5).to(device)
+    r0 = (torch.randn(M, D, generator=g) * 2).to(device)
+    lw, lb = (torch.randn(D, generator=g) * 0.5 + 1).to(device), torch.randn(D, generator=g).to(device)
+    tw, tb = torch.randn(D, generator=g).to(device), torch.randn(D, generator=g).to(device)
+    r1 = r0.clone()
+    xln, tp = ops.linear_resid_ln(a, w, bias, ls, r1, lw, lb, 1e-6, tap_w=tw if tap else None,
+                                  tap_b=tb if tap else None)
+    r2 = r0.clone()
+    ops.linear(a, w, bias=bias, scale=ls, out=r2, kind=ops.EPI_RESID, bn=256)
+    ref = ops.layernorm(r2, lw, lb, 1e-6, tw, tb) if tap else ops.layernorm(r2, lw, lb, 1e-6)
+    torch.cuda.synchronize()
+    assert torch.equal(r1, r2)
+    refs = ref if tap else (ref,)
+    outs = (xln, tp) if tap else (xln,)
+    for o, rr in zip(outs, refs):
+        d = (o.float() - rr.float()).abs()
+        assert (d <= rr.float().abs() * 2 ** -7 + 1e-5).all(), d.max().item()

@@ -53,6 +53,19 @@ def main():
     args = p.parse_args()
     dev = torch.device("cuda")
     res = []
+    if args.only == "rln":  # residual GEMM + LayerNorm kernel vs the GEMM with LN in its epilogue
+        M, D = 16400, 384
+        for K in (384, 1536):
+            a = torch.randn(M, K, device=dev).to(torch.bfloat16)
+            w = (torch.randn(D, K, device=dev) * 0.05).to(torch.bfloat16)
+            bias, ls = torch.zeros(D, device=dev), torch.ones(D, device=dev) * 0.1
+            lw, lb = torch.ones(D, device=dev), torch.zeros(D, device=dev)
+            resid = torch.randn(M, D, device=dev)
+            t_g = timeit_graph(lambda: _ops.linear(a, w, bias=bias, scale=ls, out=resid, kind=_ops.EPI_RESID, bn=256))
+            t_ln = timeit_graph(lambda: _ops.layernorm(resid, lw, lb))
+            t_f = timeit_graph(lambda: _ops.linear_resid_ln(a, w, bias, ls, resid, lw, lb, 1e-6))
+            print(json.dumps(dict(K=K, gemm_resid_us=t_g, layernorm_us=t_ln, fused_us=t_f)), flush=True)
+        return
     if args.only == "ln":  # LayerNorm + GEMM vs the GEMM with LayerNorm in its prologue
         M, D = 16400, 384
         x = torch.randn(M, D, device=dev)
