@@ -68,3 +68,29 @@ def test_backbone_batch16_fused_resid_ln(device, monkeypatch):
     # the two paths round LayerNorm sums differently, so identical taps would mean the fused
     # kernel never ran
     assert any(not torch.equal(f, p) for f, p in zip(fused, plain))
+
+
+def test_patch_im2col_block8_matches_generic(device, monkeypatch):
+    """The 8-patch-per-block im2col (448: h = 32) writes exactly what the one-block-per-patch
+    kernel writes: identical taps."""
+    from paper_2508_11584_b200.backbone import Backbone
+    R, B = 448, 2
+    cfg = model_config("vits14")
+    W = make_weights("vits14", heads=())
+    frames = make_frames(B, R, 6)
+    T = tokens(R)
+
+    def run():
+        bb = Backbone(W, cfg.backbone, R, B, device)
+        taps = [torch.empty(B, T, cfg.backbone.dim, device=device, dtype=torch.bfloat16) for _ in range(4)]
+        bb.forward(frames.to(device), taps)
+        torch.cuda.synchronize()
+        bb.close()
+        return taps
+
+    monkeypatch.delenv("VPE_IM2COL_GENERIC", raising=False)
+    a = run()
+    monkeypatch.setenv("VPE_IM2COL_GENERIC", "1")
+    b = run()
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
