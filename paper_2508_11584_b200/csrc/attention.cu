@@ -548,7 +548,11 @@ int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, in
   // fixed MMA/pipeline share; heavy units first, each to the least-loaded CTA. Round-robin left
   // T = 1025 at 3 full pairs + 1 tail unit on 36 CTAs (the tail pair holds one valid row).
   static std::map<std::tuple<int, int, int, int>, int*> cache;  // (B*heads, T, grid) -> device schedule
-  const auto key = std::make_tuple(BH, T, a->grid, 0);
+  // fixed share of a Q tile: a tile with one valid row still runs the whole KV loop (S MMAs, the
+  // pipeline, the softmax of its active warps). Calibrated with VPE_ATT_FIX over B = 4..24 at
+  // T = 1025: 0.35 left batch 12 at 95 us (8 CTAs with one full pair + 6 tail units), 0.75 -> 60 us.
+  static const double fix = getenv("VPE_ATT_FIX") ? atof(getenv("VPE_ATT_FIX")) : 0.75;
+  const auto key = std::make_tuple(BH, T, a->grid, (int)(fix * 1000));
   auto it = cache.find(key);
   if (it == cache.end()) {
     std::vector<std::pair<double, int>> cost(units);
@@ -557,7 +561,7 @@ int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, in
       double c = 0;
       for (int t = 0; t < 2; ++t) {
         const int rows = std::min(128, std::max(0, T - (q0 + 128 * t)));
-        if (rows > 0) c += 0.35 + 0.65 * rows / 128.0;
+        if (rows > 0) c += fix + (1.0 - fix) * rows / 128.0;
       }
       cost[u] = {c, u};
     }
