@@ -188,21 +188,23 @@ struct AttnUnit {
   int b, h, q0, has_b;
 };
 
-VPE_DEV AttnUnit unit_of(int u, int BH, int heads, int T) {
-  // pair-major ordering: every (image, head) pair-0 first, ..., so the (cheap) tail pairs run last
+VPE_DEV AttnUnit unit_of(int u, int BH, int heads, int T, int single) {
+  // pair-major ordering: every (image, head) pair-0 first, ..., so the (cheap) tail pairs run last.
+  // single: a unit is one 128-row Q tile (slot B never used)
   AttnUnit r;
   const int pair = u / BH, bh = u - pair * BH;
   r.b = bh / heads;
   r.h = bh - r.b * heads;
-  r.q0 = pair * 256;
-  r.has_b = (r.q0 + 128) < T;
+  r.q0 = pair * (single ? 128 : 256);
+  r.has_b = !single && (r.q0 + 128) < T;
   return r;
 }
 
 template <int POLY>
 __global__ void __launch_bounds__(ATT_THREADS, 1)
     attention_tc_kernel(const __grid_constant__ CUtensorMap tqkv, __nv_bfloat16* __restrict__ out, int B, int T,
-                        int D, int heads, float scale_log2, int trace, const int* __restrict__ sched) {
+                        int D, int heads, float scale_log2, int trace, const int* __restrict__ sched,
+                        int single) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;               // [2 units][2 slots]: the next unit's Q lands during this one
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     if (lane == 0) {
       int kit = 0, vit = 0, qn = 0;
       for (int ui = u_lo; ui < u_hi; ++ui, ++qn) {
-        const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T);
+        const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T, single);
         const int row0 = w.b * T;
         const int qb = qn & 1;
         for (int x = 0; x < 1 + w.has_b; ++x) {
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       int kit = 0, vit = 0, qn = 0, np = 0;  // np: PV MMAs issued (= p_full / s_free phases consumed)
       const uint32_t s_t = tmem + S_COL + x * 128, p_t = tmem + P_COL + x * 64, o_t = tmem + O_COL + x * 64;
       for (int ui = u_lo; ui < u_hi; ++ui, ++qn) {
-        const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T);
+        const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T, single);
         const bool mine = (x == 0) || w.has_b;
         const int qi = (qn & 1) * 2 + x;
         if (mine) {
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     const int tbase = 2048 + 1024 * x;
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
     for (int ui = u_lo; ui < u_hi; ++ui) {
-      const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T);
+      const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T, single);
       if (x == 1 && !w.has_b) continue;
       const int q0 = w.q0 + x * 128;
       const bool warp_active = (q0 + quad * 32) < T;
@@ -540,7 +542,11 @@ int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, in
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int BH = B * heads, npairs = (T + 255) / 256, units = BH * npairs;
+  const int BH = B * heads, npairs = (T + 255) / 256;
+  // small batches: pairs of Q tiles would leave most SMs idle, so run one tile per unit
+  const char* es = getenv("VPE_ATT_SINGLE");
+  a->single = es ? (es[0] == '1') : (2 * BH * npairs <= sms);
+  const int per = a->single ? (T + 127) / 128 : npairs, units = BH * per;
   a->grid = units < sms ? units : sms;
   const char* e = getenv("VPE_ATT_GRID");  // experiment: "all" = one unit per CTA (no persistence)
   if (e && e[0] == 'a') a->grid = units;
@@ -552,14 +558,14 @@ int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, in
   // pipeline, the softmax of its active warps). Calibrated with VPE_ATT_FIX over B = 4..24 at
   // T = 1025: 0.35 left batch 12 at 95 us (8 CTAs with one full pair + 6 tail units), 0.75 -> 60 us.
   static const double fix = getenv("VPE_ATT_FIX") ? atof(getenv("VPE_ATT_FIX")) : 0.75;
-  const auto key = std::make_tuple(BH, T, a->grid, (int)(fix * 1000));
+  const auto key = std::make_tuple(BH, T, a->grid, (int)(fix * 1000) * 2 + a->single);
   auto it = cache.find(key);
   if (it == cache.end()) {
     std::vector<std::pair<double, int>> cost(units);
     for (int u = 0; u < units; ++u) {
-      const int q0 = (u / BH) * 256;
+      const int q0 = (u / BH) * (a->single ? 128 : 256);
       double c = 0;
-      for (int t = 0; t < 2; ++t) {
+      for (int t = 0; t < (a->single ? 1 : 2); ++t) {
         const int rows = std::min(128, std::max(0, T - (q0 + 128 * t)));
         if (rows > 0) c += fix + (1.0 - fix) * rows / 128.0;
       }
@@ -626,7 +632,7 @@ int launch_attention(const AttnPlan& a, cudaStream_t s) {
     ~Restore() { pdl_scope() = v; }
   } restore{saved_scope};
   return launch_k(k, dim3(a.grid), dim3(ATT_THREADS), SMEM_ATT, s, a.tqkv, a.out, a.B, a.T, a.D, a.heads, scale_log2,
-                  g_att_trace_on, a.sched) == cudaSuccess
+                  g_att_trace_on, a.sched, a.single) == cudaSuccess
              ? VPE_OK
              : VPE_E_CUDA;
 }
