@@ -75,19 +75,40 @@ __global__ void __launch_bounds__(DET_THREADS) det_1x1_kernel(const float* __res
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) acc[i][j] = 0.f;
-  for (int k0 = 0; k0 < D; k0 += KT) {
+  // the next K chunk's hidden / weight values are loaded into registers while this chunk's FMAs
+  // run (one global round trip per chunk was the kernel's critical path: 12 chunks at D = 384)
+  constexpr int HJ = (PX_PER_BLK * KT) / DET_THREADS, WJ = (KT * NO_PAD + DET_THREADS - 1) / DET_THREADS;
+  float hn[HJ], wn[WJ];
+  auto fetch = [&](int k0) {
 #pragma unroll
-    for (int j = 0; j < (PX_PER_BLK * KT) / DET_THREADS; ++j) {
+    for (int j = 0; j < HJ; ++j) {
       const int i = tid + DET_THREADS * j;
       const int px = i / KT, kk = i - px * KT;
       const int gp = p0 + px;
-      s_h[kk][px] = gp < npix_total ? hidden[(int64_t)gp * D + k0 + kk] : 0.f;
+      hn[j] = gp < npix_total ? hidden[(int64_t)gp * D + k0 + kk] : 0.f;
     }
-    for (int i = tid; i < KT * NO_PAD; i += DET_THREADS) {
+#pragma unroll
+    for (int j = 0; j < WJ; ++j) {
+      const int i = tid + DET_THREADS * j;
       const int kk = i / NO_PAD, o = i - kk * NO_PAD;
-      s_w[kk][o] = o < NO ? __ldg(wT + (int64_t)(k0 + kk) * NO + o) : 0.f;
+      wn[j] = (i < KT * NO_PAD && o < NO) ? __ldg(wT + (int64_t)(k0 + kk) * NO + o) : 0.f;
+    }
+  };
+  fetch(0);
+  for (int k0 = 0; k0 < D; k0 += KT) {
+#pragma unroll
+    for (int j = 0; j < HJ; ++j) {
+      const int i = tid + DET_THREADS * j;
+      const int px = i / KT, kk = i - px * KT;
+      s_h[kk][px] = hn[j];
+    }
+#pragma unroll
+    for (int j = 0; j < WJ; ++j) {
+      const int i = tid + DET_THREADS * j;
+      if (i < KT * NO_PAD) s_w[i / NO_PAD][i % NO_PAD] = wn[j];
     }
     __syncthreads();
+    if (k0 + KT < D) fetch(k0 + KT);
 #pragma unroll 8
     for (int kk = 0; kk < KT; ++kk) {
       const float4 h = *reinterpret_cast<const float4*>(&s_h[kk][pg * 4]);
