@@ -158,14 +158,17 @@ __global__ void __launch_bounds__(1024) det_topk_kernel(const float* __restrict_
   __shared__ int s_idx[KMAX];
   __shared__ uint32_t s_prefix, s_krem, s_cnt, s_ties;
   __shared__ uint32_t s_wcount[32];
+  extern __shared__ uint32_t s_okey[];  // [n] order keys: the 4 radix passes and the gathers read smem
   const int b = blockIdx.x, tid = threadIdx.x;
   const float* o = obj + (int64_t)b * n;
+  for (int i = tid; i < n; i += blockDim.x) s_okey[i] = order_key(__ldg(o + i));
+  __syncthreads();
   uint32_t prefix = 0, pmask = 0, krem = K;
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     for (int i = tid; i < n; i += blockDim.x) {
-      const uint32_t k = order_key(o[i]);
+      const uint32_t k = s_okey[i];
       if ((k & pmask) == prefix) atomicAdd(&hist[(k >> shift) & 255], 1u);
     }
     __syncthreads();
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(1024) det_topk_kernel(const float* __restrict_
   }
   __syncthreads();
   for (int i = tid; i < n; i += blockDim.x) {
-    const uint32_t k = order_key(o[i]);
+    const uint32_t k = s_okey[i];
     if (k > prefix) {
       const uint32_t pos = atomicAdd(&s_cnt, 1u);
       s_key[pos] = k;
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(1024) det_topk_kernel(const float* __restrict_
   const uint32_t gcount = K - krem;
   for (int base = 0; base < n; base += blockDim.x) {
     const int i = base + tid;
-    const bool tie = (i < n) && order_key(o[i]) == prefix;
+    const bool tie = (i < n) && s_okey[i] == prefix;
     const uint32_t bal = __ballot_sync(0xffffffffu, tie);
     if ((tid & 31) == 0) s_wcount[tid >> 5] = __popc(bal);
     __syncthreads();
@@ -485,7 +488,14 @@ extern "C" int vpe_det_forward(vpe_det* d, const void* final_tap, const vpe_det_
   det_1x1_kernel<<<(npix + PX_PER_BLK - 1) / PX_PER_BLK, DET_THREADS, 0, st>>>(d->hidden, npix, d->P, D, A, d->wT, d->bcat, d->obj,
                                                          d->deltas);
   VPE_CUDA_TRY(cudaGetLastError());
-  det_topk_kernel<<<B, 1024, 0, st>>>(d->obj, d->deltas, n, K, d->cfg, h, d->cbox, d->cscore, d->cidx, d->cvalid,
+  const size_t topk_smem = (size_t)n * 4;
+  static bool topk_attr = false;
+  if (!topk_attr) {
+    VPE_CUDA_TRY(cudaFuncSetAttribute(det_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    topk_attr = true;
+  }
+  if (topk_smem > 160 * 1024) return VPE_E_CONFIG;
+  det_topk_kernel<<<B, 1024, topk_smem, st>>>(d->obj, d->deltas, n, K, d->cfg, h, d->cbox, d->cscore, d->cidx, d->cvalid,
                                       o->top_index);
   VPE_CUDA_TRY(cudaGetLastError());
   const int nb = (K + NMS_BLK - 1) / NMS_BLK;
