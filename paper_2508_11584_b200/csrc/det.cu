@@ -246,26 +246,40 @@ __global__ void __launch_bounds__(1024) det_topk_kernel(const float* __restrict_
     s_idx[i] = 0x7fffffff;
   }
   __syncthreads();
-  // bitonic sort, descending key, ascending index on ties
-  for (int k = 2; k <= KMAX; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < KMAX; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const uint32_t ka = s_key[i], kb = s_key[ixj];
-          const int ia = s_idx[i], ib = s_idx[ixj];
-          const bool a_first = (ka > kb) || (ka == kb && ia < ib);
-          const bool up = (i & k) == 0;
-          if (up ? !a_first : a_first) {
-            s_key[i] = kb;
-            s_key[ixj] = ka;
-            s_idx[i] = ib;
-            s_idx[ixj] = ia;
-          }
+  // bitonic sort, descending key, ascending index on ties. One element per thread (blockDim ==
+  // KMAX); partners closer than a warp exchange by shuffle, the 15 wider stages through smem
+  // (55 block-wide barriers -> 30)
+  {
+    uint32_t key = s_key[tid];
+    int idx = s_idx[tid];
+    for (int k = 2; k <= KMAX; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        uint32_t pk;
+        int pi;
+        if (j >= 32) {
+          __syncthreads();
+          s_key[tid] = key;
+          s_idx[tid] = idx;
+          __syncthreads();
+          pk = s_key[tid ^ j];
+          pi = s_idx[tid ^ j];
+        } else {
+          pk = __shfl_xor_sync(0xffffffffu, key, j);
+          pi = __shfl_xor_sync(0xffffffffu, idx, j);
+        }
+        const bool up = (tid & k) == 0, lower = (tid & j) == 0;
+        const bool self_first = (key > pk) || (key == pk && idx < pi);
+        const bool take = (lower == up) ? !self_first : self_first;
+        if (take) {
+          key = pk;
+          idx = pi;
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
+    s_key[tid] = key;
+    s_idx[tid] = idx;
+    __syncthreads();
   }
   // decode (torchvision _utils.py:183-225) + clip + remove small + sigmoid
   const int A = cfg.num_anchors;
