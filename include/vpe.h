@@ -20,6 +20,7 @@
  *   vpe_ring_pop                              <- channels.py:377-421
  *   vpe_ring_counters                         <- channels.py:493-504
  *   vpe_copy_counter                          <- arena.py:190-219
+ *   vpe_region_* / vpe_copy_out               <- arena.py:285-373    (create/attach_region, copy_out)
  *   vpe_vit_* / vpe_dpt_* / vpe_seg_* / vpe_det_* <- SPEC.md:232-243 ComputeBackend.infer
  *        (the reference has no NN code; these are the backend descriptors "b200_vit",
  *         "b200_dpt", "b200_linseg", "b200_det" that stand in for TensorRT engines)
@@ -126,11 +127,28 @@ int vpe_ring_commit(vpe_ring* r, vpe_lease* lease, void* stream);
 int vpe_ring_consume(vpe_ring* r, vpe_lease* lease, const int32_t* labels, int32_t nlabels, void* const* dst,
                      void* stream);
 int vpe_ring_release(vpe_ring* r, vpe_lease* lease, void* stream);
-/* FIFO: oldest READY frame copied into dst (all labels, stream-ordered), slot FREE after copy */
-int vpe_ring_pop(vpe_ring* r, uint32_t consumer_id, void* const* dst, void* stream, vpe_lease* envelope);
+/* FIFO: oldest READY frame copied into dst (all labels), slot FREE after copy. dst_on_host != 0:
+ * dst are host pointers, the call waits for the producer's ready event and copies synchronously;
+ * otherwise dst are device pointers and the copies are ordered on `stream` (NULL = the legacy
+ * default stream). Streams are never NULL-tested: NULL is a valid stream for every entry point. */
+int vpe_ring_pop(vpe_ring* r, uint32_t consumer_id, void* const* dst, int32_t dst_on_host, void* stream,
+                 vpe_lease* envelope);
 int vpe_ring_counters(vpe_ring* r, vpe_counters* c);
 int vpe_ring_slot_state(vpe_ring* r, int32_t slot, uint32_t* state, uint64_t* frame_id);
 int64_t vpe_copy_counter(void);
+
+/* ---- shareable regions (arena.py:285-413 create_region / attach_region / copy_out) ----
+ * name = "<namespace>.<region>"; a POSIX segment "/<name>" holds the bytes (VPE_HOST_PLAIN) or a
+ * descriptor of the HBM allocation exported through CUDA IPC (device >= 0). Zero-initialised.
+ * Errors: AlreadyExists / NotFound / CorruptHandle (attach with expect_bytes > region size). */
+typedef struct vpe_region vpe_region;
+int vpe_region_create(const char* name, uint64_t nbytes, int32_t device, vpe_region** out);
+int vpe_region_attach(const char* name, uint64_t expect_bytes, vpe_region** out);
+int vpe_region_info(vpe_region* region, void** base, uint64_t* nbytes, int32_t* device);
+int vpe_region_destroy(vpe_region* region, int32_t unlink_segment);
+/* the single permitted copy (copy counter +1): host memcpy, or stream-ordered cudaMemcpyAsync
+ * when either side is device memory (host_sync != 0: wait for it) */
+int vpe_copy_out(void* dst, const void* src, uint64_t nbytes, void* stream, int32_t host_sync);
 
 /* ---- backbone: DINOv2 ViT forward writing 4 tap features (bf16 [B,T,D]) ---- */
 #define VPE_MAX_LAYERS 40
@@ -256,14 +274,7 @@ int vpe_det_forward(vpe_det* d, const void* final_tap, const vpe_det_outputs* ou
  * 3 f32. Kw may be a multiple of K (split-precision weights, A repeated). */
 int vpe_op_linear(const void* A, int32_t M, int32_t K, const void* W, int32_t N, int32_t Kw, const float* bias,
                   const float* scale, void* out, int32_t kind, int32_t act, int32_t bn, void* stream);
-/* bn > 0: one-CTA 128 x bn tiles; bn < 0: CTA-pair (cta_group::2) 256 x |bn| tiles */
-/* camera ingest alone: [B,H,W,3] u8 -> normalised bf16 patch rows [B*(R/14)^2, 640] (k = c*196+ky*14+kx) */
-/* out bf16 [M, N] = act(LayerNorm(x) W^T + bias) with the LayerNorm (x fp32 [M, D], D = 384)
- * computed inside the GEMM; optional tap_out bf16 [M, D] = LayerNorm with (tap_w, tap_b)
- * (DINOv2 block norm1 -> attention.qkv / norm2 -> mlp.fc1: modeling_dinov2.py:382-420) */
-int vpe_op_linear_ln(const float* x, int32_t M, int32_t D, const float* ln_w, const float* ln_b, float eps,
-                     const float* tap_w, const float* tap_b, void* tap_out, const void* W, int32_t N, const float* bias,
-                     int32_t act, void* out, void* stream);
+/* bn: 128 x bn tiles (32, 64, 128, 192, 256) */
 /* resid fp32 [M, 384] += ls * (A W^T + bias), A bf16 [M, K], W bf16 [384, K]; then xln bf16 =
  * LayerNorm(resid) (ln_w, ln_b) and optionally tap_out = LayerNorm(resid) (tap_w, tap_b), in the
  * same kernel (DINOv2 block: attention.output / mlp.fc2 + layer_scale + residual, then the next
@@ -271,6 +282,7 @@ int vpe_op_linear_ln(const float* x, int32_t M, int32_t D, const float* ln_w, co
 int vpe_op_linear_resid_ln(const void* A, int32_t M, int32_t K, const void* W, const float* bias, const float* ls,
                            float* resid, const float* ln_w, const float* ln_b, float eps, void* xln, const float* tap_w,
                            const float* tap_b, void* tap_out, void* stream);
+/* camera ingest alone: [B,H,W,3] u8 -> normalised bf16 patch rows [B*(R/14)^2, 640] (k = c*196+ky*14+kx) */
 int vpe_op_camera_im2col(const void* frames_hwc_u8, int32_t B, int32_t height, int32_t width, int32_t resolution,
                          void* out_bf16, void* stream);
 /* 3x3 or 1x1 same-padding conv on NHWC bf16 x [B,H,W,Cp] with weights [N, ks*ks*Cp] -> out bf16 NHWC
@@ -278,10 +290,6 @@ int vpe_op_camera_im2col(const void* frames_hwc_u8, int32_t B, int32_t height, i
 int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32_t Cp, int32_t ks, const void* w,
                 int32_t N, const float* bias, const void* add1, const void* add2, void* out, void* out_relu,
                 int32_t ldo, int32_t act, void* stream);
-/* fused MLP block: resid[M,D] += ls2 * (GELU(X W1^T + b1) W2^T + b2); X bf16 [M,D], W1 bf16 [hidden,D],
- * W2 bf16 [D,hidden]; D = 384 only (VPE_E_SHAPE otherwise) */
-int vpe_op_mlp(const void* X, int32_t M, int32_t D, int32_t hidden, const void* W1, const float* b1, const void* W2,
-               const float* b2, const float* ls2, float* resid, void* stream);
 int vpe_op_attention(const void* qkv, void* out, int32_t B, int32_t T, int32_t D, int32_t heads, void* stream);
 /* bilinear (align_corners=False) upsample of fp32 logits [B, h*h, cp] (C real classes) to
  * [B, R, R] + argmax over classes -> u8 labels; R = 14 h; torch's rounding and first-index ties
@@ -306,6 +314,7 @@ int vpe_graph_launch(vpe_graph* g, void* stream);
 int vpe_graph_destroy(vpe_graph* g);
 int vpe_event_create(void** ev);
 int vpe_event_record(void* ev, void* stream);
+int vpe_event_sync(void* ev);   /* host waits for the event (GIL released by ctypes) */
 int vpe_event_elapsed_ms(void* start, void* end, float* ms);
 int vpe_event_destroy(void* ev);
 int vpe_stream_wait_event(void* stream, void* ev);
@@ -319,7 +328,6 @@ const char* vpe_status_str(int status);
    ((code, clock64) pairs; see csrc/attention.cu) */
 int vpe_debug_att_trace(unsigned long long* host, int32_t n);
 int vpe_debug_gemm_trace(unsigned long long* host, int32_t n);
-int vpe_debug_mlp_trace(unsigned long long* host, int32_t n);
 
 #ifdef __cplusplus
 }

@@ -118,10 +118,15 @@ _SIGS = {
     "vpe_ring_commit": (i32, [vp, C.POINTER(LeaseC), vp]),
     "vpe_ring_consume": (i32, [vp, C.POINTER(LeaseC), C.POINTER(i32), i32, C.POINTER(vp), vp]),
     "vpe_ring_release": (i32, [vp, C.POINTER(LeaseC), vp]),
-    "vpe_ring_pop": (i32, [vp, u32, C.POINTER(vp), vp, C.POINTER(LeaseC)]),
+    "vpe_ring_pop": (i32, [vp, u32, C.POINTER(vp), i32, vp, C.POINTER(LeaseC)]),
     "vpe_ring_counters": (i32, [vp, C.POINTER(CountersC)]),
     "vpe_ring_slot_state": (i32, [vp, i32, C.POINTER(u32), C.POINTER(u64)]),
     "vpe_copy_counter": (i64, []),
+    "vpe_region_create": (i32, [C.c_char_p, u64, i32, C.POINTER(vp)]),
+    "vpe_region_attach": (i32, [C.c_char_p, u64, C.POINTER(vp)]),
+    "vpe_region_info": (i32, [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(i32)]),
+    "vpe_region_destroy": (i32, [vp, i32]),
+    "vpe_copy_out": (i32, [vp, vp, u64, vp, i32]),
     # models
     "vpe_vit_create": (i32, [C.POINTER(VitConfigC), C.POINTER(VitWeightsC), C.POINTER(vp)]),
     "vpe_vit_destroy": (i32, [vp]),
@@ -144,11 +149,8 @@ _SIGS = {
     "vpe_set_pdl": (i32, [i32]),
     "vpe_debug_att_trace": (i32, [vp, i32]),
     "vpe_debug_gemm_trace": (i32, [vp, i32]),
-    "vpe_debug_mlp_trace": (i32, [vp, i32]),
     "vpe_op_attention": (i32, [vp, vp, i32, i32, i32, i32, vp]),
-    "vpe_op_mlp": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
     "vpe_op_linear_resid_ln": (i32, [vp, i32, i32, vp, vp, vp, vp, vp, vp, f32, vp, vp, vp, vp, vp]),
-    "vpe_op_linear_ln": (i32, [vp, i32, i32, vp, vp, f32, vp, vp, vp, vp, i32, vp, i32, vp, vp]),
     "vpe_op_bilinear": (i32, [vp, i32, i32, i32, i32, i32, vp, i32, i32, vp]),
     "vpe_op_upsample_argmax": (i32, [vp, i32, i32, i32, i32, i32, vp, vp]),
     "vpe_op_layernorm": (i32, [vp, i32, i32, vp, vp, f32, vp, vp, vp, vp, vp]),
@@ -162,6 +164,7 @@ _SIGS = {
     "vpe_graph_destroy": (i32, [vp]),
     "vpe_event_create": (i32, [C.POINTER(vp)]),
     "vpe_event_record": (i32, [vp, vp]),
+    "vpe_event_sync": (i32, [vp]),
     "vpe_event_elapsed_ms": (i32, [vp, vp, C.POINTER(f32)]),
     "vpe_event_destroy": (i32, [vp]),
     "vpe_stream_wait_event": (i32, [vp, vp]),

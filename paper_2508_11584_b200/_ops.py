@@ -60,19 +60,6 @@ def layernorm(x: torch.Tensor, w, b, eps=1e-6, w2=None, b2=None, stream=None):
     return out if out2 is None else (out, out2)
 
 
-def linear_ln(x: torch.Tensor, ln_w, ln_b, eps: float, w: torch.Tensor, bias=None, act=ACT_NONE,
-              tap_w=None, tap_b=None, stream=None):
-    """act(LayerNorm(x) @ w.T + bias), LayerNorm inside the GEMM; x fp32 [M, 384]. Returns
-    (out bf16 [M, N], tap bf16 [M, 384] or None)."""
-    M, D = x.shape
-    N = w.shape[0]
-    out = torch.empty(M, N, device=x.device, dtype=torch.bfloat16)
-    tap = torch.empty(M, D, device=x.device, dtype=torch.bfloat16) if tap_w is not None else None
-    check(lib.vpe_op_linear_ln(_p(x), M, D, _p(ln_w), _p(ln_b), eps, _p(tap_w), _p(tap_b), _p(tap), _p(w), N,
-                               _p(bias), act, _p(out), _s(stream)), "vpe_op_linear_ln")
-    return out, tap
-
-
 def linear_resid_ln(a: torch.Tensor, w: torch.Tensor, bias, ls, resid: torch.Tensor, ln_w, ln_b, eps: float,
                     tap_w=None, tap_b=None, stream=None):
     """resid += ls * (a @ w.T + bias) in place; returns (LayerNorm(resid) bf16, tap bf16 or None)."""
@@ -110,12 +97,3 @@ def camera_im2col(frames_hwc: torch.Tensor, resolution: int, stream=None) -> tor
     out = torch.empty(n, 640, device=frames_hwc.device, dtype=torch.bfloat16)
     check(lib.vpe_op_camera_im2col(_p(frames_hwc), B, H, W, resolution, _p(out), _s(stream)), "vpe_op_camera_im2col")
     return out
-
-
-def mlp(x: torch.Tensor, w1: torch.Tensor, b1: torch.Tensor, w2: torch.Tensor, b2: torch.Tensor,
-        ls2: torch.Tensor, resid: torch.Tensor, stream=None) -> torch.Tensor:
-    """Fused MLP block, in place: resid += ls2 * (GELU(x w1^T + b1) w2^T + b2)."""
-    M, D = x.shape
-    check(lib.vpe_op_mlp(_p(x), M, D, w1.shape[0], _p(w1), _p(b1), _p(w2), _p(b2), _p(ls2), _p(resid), _s(stream)),
-          "vpe_op_mlp")
-    return resid

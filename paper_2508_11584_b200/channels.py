@@ -4,7 +4,7 @@ ring (``vpe_ring_*``, include/vpe.h).
 Same names, arguments, outcomes and exceptions as the reference: ``create_channel``,
 ``Channel.push / register_consumer / acquire_latest / consume / release / pop / counters /
 slot_states / group_views / last_consumed``, ``ChannelHandle``, ``SlotGroup``,
-``create_processing_slots``, ``PushKind`` / ``PushOutcome`` / ``Lease`` / ``FrameEnvelope`` /
+``create_processing_slots`` / ``open_processing_slots``, ``PushKind`` / ``PushOutcome`` / ``Lease`` / ``FrameEnvelope`` /
 ``ChannelCounters``. The control block keeps the PECH1 byte layout; the state machine runs in
 C++ with the reference's CAS protocol.
 
@@ -113,44 +113,67 @@ class ChannelHandle:
 
 
 class SlotGroup:
-    """Caller-owned processing slots: one tensor per label (consume/pop destinations)."""
+    """Caller-owned processing slots: one arena slot per channel label (channels.py:155-176)."""
 
-    def __init__(self, tensors: Mapping[str, torch.Tensor], specs: Mapping[str, ar.TensorSpec]):
-        self._t = dict(tensors)
-        self._specs = dict(specs)
+    def __init__(self, accessor, refs: Mapping[str, ar.SlotRef]):
+        self.arena = accessor
+        self.refs = dict(refs)
+        self._views = {lbl: accessor.data_view(ref.offset, ref.spec) for lbl, ref in self.refs.items()}
 
     @property
     def labels(self) -> tuple[str, ...]:
-        return tuple(self._t)
+        return tuple(self.refs)
 
-    @property
-    def refs(self) -> dict[str, torch.Tensor]:
-        return self._t
+    def ref(self, label: str) -> ar.SlotRef:
+        return self.refs[label]
 
     def view(self, label: str) -> torch.Tensor:
-        return self._t[label]
+        return self._views[label]
 
     def spec(self, label: str) -> ar.TensorSpec:
-        return self._specs[label]
+        return self.refs[label].spec
+
+
+class _PinnedArena:
+    """A process-private arena in pinned host memory (D2H destinations of output queues)."""
+
+    def __init__(self, handle: ar.ShareHandle):
+        self.handle = handle
+        self.device = -1
+        self.buf = torch.zeros(handle.total_bytes, dtype=torch.uint8, pin_memory=torch.cuda.is_available())
+
+    def data_view(self, offset: int, spec: ar.TensorSpec) -> torch.Tensor:
+        return ar.view_of(self.buf, offset, spec)
+
+    def close(self) -> None:
+        self.buf = None
+
+
+def _refs(handle: ar.ShareHandle, layout: ar.ArenaLayout) -> dict[str, ar.SlotRef]:
+    return {spec.label: ar.SlotRef(handle, sid, spec, layout.offset_of(sid)) for sid, spec in layout.slots}
 
 
 def create_processing_slots(namespace: str, region_name: str, specs: Sequence[ar.TensorSpec],
                             device: int | str = 0) -> SlotGroup:
-    """Preallocate a consumer-private destination group (device, or pinned host with device=-1)."""
-    ar.validate_name("namespace", namespace)
-    ar.validate_name("region_name", region_name)
+    """Preallocate a consumer-private destination group for consume()/pop() (channels.py:179-186):
+    an arena in HBM (device >= 0) or POSIX shared memory (-2 / "cpu"), both shareable through
+    ``open_processing_slots``, or private pinned host memory (-1 / "host")."""
+    dev = {"host": -1, "cpu": -2}.get(device, device) if isinstance(device, str) else int(device)
     layout = ar.ArenaLayout.from_specs(list(specs))
-    ar.log_allocation(f"{namespace}.{region_name}", layout.total_bytes)
-    tens = {}
-    for s in specs:
-        if device == -1 or device == "host":
-            t = torch.empty(s.dims, dtype=s.dtype.torch_dtype, pin_memory=torch.cuda.is_available())
-        elif device == -2 or device == "cpu":
-            t = torch.empty(s.dims, dtype=s.dtype.torch_dtype)
-        else:
-            t = torch.empty(s.dims, dtype=s.dtype.torch_dtype, device=f"cuda:{int(device)}")
-        tens[s.label] = t
-    return SlotGroup(tens, {s.label: s for s in specs})
+    if dev == -1:
+        ar.validate_name("namespace", namespace)
+        ar.validate_name("region_name", region_name)
+        handle = ar.ShareHandle(namespace, region_name, layout.total_bytes, -1)
+        ar.log_allocation(handle.os_name, layout.total_bytes)
+        return SlotGroup(_PinnedArena(handle), _refs(handle, layout))
+    accessor, handle = ar.create_arena(layout, namespace, region_name, device=dev)
+    return SlotGroup(accessor, _refs(handle, layout))
+
+
+def open_processing_slots(handle: ar.ShareHandle, specs: Sequence[ar.TensorSpec]) -> SlotGroup:
+    """Map another process's processing slots (channels.py:189-196)."""
+    accessor = ar.import_arena(handle)
+    return SlotGroup(accessor, _refs(handle, ar.ArenaLayout.from_specs(list(specs))))
 
 
 class _Backoff:
@@ -308,6 +331,10 @@ class Channel:
         if unknown:
             raise LabelError(f"labels {unknown} not in channel label set {self.labels}")
 
+    @staticmethod
+    def _dst_tensor(dst, label):
+        return dst.view(label) if isinstance(dst, SlotGroup) else dst[label]
+
     def _check_dst(self, dst: SlotGroup | Mapping[str, torch.Tensor], labels) -> list[int]:
         ptrs = []
         for lbl in labels:
@@ -331,8 +358,11 @@ class Channel:
         ptrs = self._check_dst(dst, chosen)
         idx = (C.c_int32 * len(chosen))(*[self._label_idx[lbl] for lbl in chosen])
         pp = (C.c_void_p * len(chosen))(*ptrs)
-        check(lib.vpe_ring_consume(self._ring, C.byref(lease._c), idx, len(chosen), pp, _sp(self._s(stream))),
-              "consume")
+        s = self._s(stream)
+        check(lib.vpe_ring_consume(self._ring, C.byref(lease._c), idx, len(chosen), pp, _sp(s)), "consume")
+        if self.device != -2 and any(not self._dst_tensor(dst, l).is_cuda for l in chosen):
+            # host destinations: the reference's consume returns with the bytes in dst
+            check(lib.vpe_stream_sync(_sp(s)), "consume")
         lease.consumed = True
         return FrameEnvelope(lease.frame_id, lease.capture_ts, chosen)
 
@@ -353,13 +383,16 @@ class Channel:
         self._require(consumer_id)
         ptrs = self._check_dst(dst, self.labels)
         pp = (C.c_void_p * len(ptrs))(*ptrs)
-        host_dst = all(not (dst.view(l) if isinstance(dst, SlotGroup) else dst[l]).is_cuda for l in self.labels)
-        s = None if host_dst else self._s(stream)
+        on_dev = [(dst.view(l) if isinstance(dst, SlotGroup) else dst[l]).is_cuda for l in self.labels]
+        if any(on_dev) and not all(on_dev):
+            raise ShapeError("pop destinations must be all host or all device tensors")
+        host_dst = not any(on_dev)
+        s = self._s(stream)
         backoff = _Backoff()
         deadline = None if timeout is None else time.monotonic() + timeout
         env = LeaseC()
         while True:
-            rc = lib.vpe_ring_pop(self._ring, consumer_id, pp, _sp(s), C.byref(env))
+            rc = lib.vpe_ring_pop(self._ring, consumer_id, pp, int(host_dst), _sp(s), C.byref(env))
             if rc != NO_NEW_DATA:
                 check(rc, "pop")
                 return FrameEnvelope(int(env.frame_id), int(env.capture_ts), self.labels)

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <tuple>
 #include <utility>
 #include <vector>
@@ -553,12 +554,15 @@ int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, in
   // Longest-processing-time-first static schedule: a unit costs ~ its Q tiles' valid rows plus a
   // fixed MMA/pipeline share; heavy units first, each to the least-loaded CTA. Round-robin left
   // T = 1025 at 3 full pairs + 1 tail unit on 36 CTAs (the tail pair holds one valid row).
-  static std::map<std::tuple<int, int, int, int>, int*> cache;  // (B*heads, T, grid) -> device schedule
+  // (device, B*heads, T, grid, mode) -> device schedule; the schedule array lives on that device
+  static std::map<std::tuple<int, int, int, int, int>, int*> cache;
+  static std::mutex cache_mu;
   // fixed share of a Q tile: a tile with one valid row still runs the whole KV loop (S MMAs, the
   // pipeline, the softmax of its active warps). Calibrated with VPE_ATT_FIX over B = 4..24 at
   // T = 1025: 0.35 left batch 12 at 95 us (8 CTAs with one full pair + 6 tail units), 0.75 -> 60 us.
   static const double fix = getenv("VPE_ATT_FIX") ? atof(getenv("VPE_ATT_FIX")) : 0.75;
-  const auto key = std::make_tuple(BH, T, a->grid, (int)(fix * 1000) * 2 + a->single);
+  const auto key = std::make_tuple(dev, BH, T, a->grid, (int)(fix * 1000) * 2 + a->single);
+  std::lock_guard<std::mutex> lock(cache_mu);
   auto it = cache.find(key);
   if (it == cache.end()) {
     std::vector<std::pair<double, int>> cost(units);
@@ -603,6 +607,9 @@ int launch_attention(const AttnPlan& a, cudaStream_t s) {
   if (poly < 0) {
     const char* e = getenv("VPE_ATT_POLY");
     poly = e ? atoi(e) : 3;  // 4 of 16 pairs on the FMA pipe (tools/ubench/emit.cu: best MUFU/FMA balance)
+  }
+  static OncePerDevice attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(attention_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
     cudaFuncSetAttribute(attention_tc_kernel<0x0707>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
     cudaFuncSetAttribute(attention_tc_kernel<0x0303>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);

@@ -4,7 +4,6 @@
 #include <new>
 
 #include "attention.cuh"
-#include "mlp.cuh"
 #include "gemm.cuh"
 #include "misc.cuh"
 #include "runtime.h"
@@ -87,23 +86,6 @@ int vpe_op_linear(const void* A, int32_t M, int32_t K, const void* W, int32_t N,
   return VPE_OK;
 }
 
-int vpe_op_linear_ln(const float* x, int32_t M, int32_t D, const float* ln_w, const float* ln_b, float eps,
-                     const float* tap_w, const float* tap_b, void* tap_out, const void* W, int32_t N, const float* bias,
-                     int32_t act, void* out, void* stream) {
-  EpiParams ep;
-  ep.kind = EPI_BF16;
-  ep.act = act;
-  ep.N = N;
-  ep.bias = bias;
-  ep.out = out;
-  ep.ldo = N;
-  GemmPlan g;
-  VPE_TRY(plan_gemm_ln(&g, x, M, D, ln_w, ln_b, eps, tap_w, tap_b, static_cast<const __nv_bfloat16*>(W), N, ep, 256));
-  VPE_TRY(launch_gemm_ln(g, static_cast<__nv_bfloat16*>(tap_out), static_cast<cudaStream_t>(stream)));
-  count_launches(1);
-  return VPE_OK;
-}
-
 int vpe_op_linear_resid_ln(const void* A, int32_t M, int32_t K, const void* W, const float* bias, const float* ls,
                            float* resid, const float* ln_w, const float* ln_b, float eps, void* xln, const float* tap_w,
                            const float* tap_b, void* tap_out, void* stream) {
@@ -146,16 +128,6 @@ int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32
 
 int vpe_set_pdl(int32_t on) {
   pdl_flag() = on ? 1 : 0;
-  return VPE_OK;
-}
-
-int vpe_op_mlp(const void* X, int32_t M, int32_t D, int32_t hidden, const void* W1, const float* b1, const void* W2,
-               const float* b2, const float* ls2, float* resid, void* stream) {
-  MlpPlan m;
-  VPE_TRY(plan_mlp(&m, static_cast<const __nv_bfloat16*>(X), M, D, hidden, static_cast<const __nv_bfloat16*>(W1), b1,
-                   static_cast<const __nv_bfloat16*>(W2), b2, ls2, resid));
-  VPE_TRY(launch_mlp(m, static_cast<cudaStream_t>(stream)));
-  count_launches(1);
   return VPE_OK;
 }
 
@@ -245,6 +217,10 @@ int vpe_event_create(void** ev) {
 }
 int vpe_event_record(void* ev, void* stream) {
   VPE_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream)));
+  return VPE_OK;
+}
+int vpe_event_sync(void* ev) {
+  VPE_CUDA_TRY(cudaEventSynchronize(static_cast<cudaEvent_t>(ev)));
   return VPE_OK;
 }
 int vpe_event_elapsed_ms(void* a, void* b, float* ms) {

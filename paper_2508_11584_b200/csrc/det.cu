@@ -21,6 +21,7 @@ using namespace vpe;
 
 namespace {
 constexpr int KMAX = 1024;  // candidate capacity (pre_nms_top_n <= 1024)
+constexpr size_t TOPK_SMEM_MAX = 160 * 1024;  // det_topk_kernel order-key cache (n * 4 bytes)
 constexpr int NMS_BLK = 64;
 constexpr int NWORDS = KMAX / NMS_BLK;  // 16 x u64 per mask row
 }  // namespace
@@ -443,6 +444,11 @@ extern "C" int vpe_det_create(const vpe_det_config* cfg, const vpe_det_weights* 
   if (cfg->resolution % 14 || cfg->dim % 64 || cfg->num_anchors < 1 || cfg->num_anchors > 9 ||
       cfg->pre_nms_top_n < 1 || cfg->pre_nms_top_n > KMAX || cfg->post_nms_top_n < 1)
     return VPE_E_CONFIG;
+  {
+    // the top-k kernel keeps one 4-byte order key per anchor in shared memory
+    const int hh = cfg->resolution / 14;
+    if ((size_t)hh * hh * cfg->num_anchors * 4 > TOPK_SMEM_MAX) return VPE_E_CONFIG;
+  }
   vpe_det* d = new (std::nothrow) vpe_det();
   if (!d) return VPE_E_RESOURCE;
   d->cfg = *cfg;
@@ -503,27 +509,24 @@ extern "C" int vpe_det_forward(vpe_det* d, const void* final_tap, const vpe_det_
                                                          d->deltas);
   VPE_CUDA_TRY(cudaGetLastError());
   const size_t topk_smem = (size_t)n * 4;
-  static bool topk_attr = false;
-  if (!topk_attr) {
-    VPE_CUDA_TRY(cudaFuncSetAttribute(det_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    topk_attr = true;
+  static OncePerDevice topk_attr;
+  if (topk_attr.first()) {
+    VPE_CUDA_TRY(cudaFuncSetAttribute(det_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TOPK_SMEM_MAX));
   }
-  if (topk_smem > 160 * 1024) return VPE_E_CONFIG;
   det_topk_kernel<<<B, 1024, topk_smem, st>>>(d->obj, d->deltas, n, K, d->cfg, h, d->cbox, d->cscore, d->cidx, d->cvalid,
                                       o->top_index);
   VPE_CUDA_TRY(cudaGetLastError());
   const int nb = (K + NMS_BLK - 1) / NMS_BLK;
   det_nms_mask_kernel<<<dim3(nb, nb, B), NMS_BLK, 0, st>>>(d->cbox, K, d->cfg.nms_thresh, d->mask);
   VPE_CUDA_TRY(cudaGetLastError());
-  static bool attr = false;
+  static OncePerDevice attr;
   const size_t smem = (size_t)K * NWORDS * 8;
-  if (!attr) {
+  if (attr.first()) {
     cudaFuncSetAttribute(det_nms_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, KMAX * NWORDS * 8);
     max_smem_carveout(det_nms_scan_kernel);
     max_smem_carveout(det_1x1_kernel);
     max_smem_carveout(det_topk_kernel);
     max_smem_carveout(det_nms_mask_kernel);
-    attr = true;
   }
   det_nms_scan_kernel<<<B, 512, smem, st>>>(d->mask, d->cvalid, d->cbox, d->cscore, d->cidx, K,
                                             d->cfg.post_nms_top_n, o->boxes, o->scores, o->index, o->count);

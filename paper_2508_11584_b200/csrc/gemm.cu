@@ -15,7 +15,6 @@
 #include <cstring>
 
 #include "gemm.cuh"
-#include "ln.cuh"
 #include "tc.cuh"
 #include "util.cuh"
 
@@ -315,9 +314,11 @@ VPE_DEV void epilogue_conv_staged(const EpiParams& ep, int64_t gpix, bool valid,
   }
 }
 
-// optional MMA-thread timeline of CTA 0 (diagnostics only: VPE_GEMM_TRACE=1, vpe_debug_gemm_trace)
+// optional MMA-thread timeline of CTA 0: a diagnostics build only (nvcc -DVPE_TRACE_BUILD, then
+// VPE_GEMM_TRACE=1 and vpe_debug_gemm_trace); the product build compiles the probes out
 __device__ unsigned long long g_gemm_trace[4096];
 static int g_gemm_trace_on = -1;
+#ifdef VPE_TRACE_BUILD
 #define GEMM_TRACE(idx, code)                                                        \
   do {                                                                               \
     if (p.trace && blockIdx.x == 0 && (idx) < 2040) {                                \
@@ -326,9 +327,15 @@ static int g_gemm_trace_on = -1;
       ++(idx);                                                                       \
     }                                                                                \
   } while (0)
+#else
+#define GEMM_TRACE(idx, code) \
+  do {                        \
+  } while (0)
+#endif
 
 // per-role variant: slots [base, base + 600) of CTA 0's timeline (halo conv: MMA 0, TMA 680,
 // epilogue warp 2 at 1360)
+#ifdef VPE_TRACE_BUILD
 #define ROLE_TRACE(base, idx, code)                                                  \
   do {                                                                               \
     if (p.trace && blockIdx.x == 0 && (idx) < 600) {                                 \
@@ -337,6 +344,11 @@ static int g_gemm_trace_on = -1;
       ++(idx);                                                                       \
     }                                                                                \
   } while (0)
+#else
+#define ROLE_TRACE(base, idx, code) \
+  do {                              \
+  } while (0)
+#endif
 
 // One 32-column chunk of a row-major tile through the TMA-store epilogue: bias / LayerScale /
 // activation in registers, swizzled smem staging (per-warp double buffer), then a TMA bulk store
@@ -555,385 +567,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           epilogue_tma_chunk(p, &tout, v, col0, m0 + q * 32, stg_base, nstore);
         } else if (valid) {
           epilogue_direct(p.ep, gpix, col0, v);
-        }
-      }
-    }
-    if (lane == 0) bulk_wait0();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, C::TMEM_COLS);
-  }
-}
-
-
-// ------------------------------------------------------------------------------------------
-// CTA-pair GEMM (cta_group::2), row-major A. A cluster of 2 CTAs on one TPC computes a
-// 256 x BN tile: each CTA stages its own 128 A rows and half (BN/2) of the B rows, the leader
-// (rank 0) issues tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' smem, and each CTA's
-// TMEM receives its 128 x BN accumulator. Per SM that halves the B traffic from L2 -- the
-// bound for these K = 384 backbone GEMMs (the 128 x BN one-CTA kernel is L2-bandwidth bound).
-//   warp 0 (both CTAs)  TMA producer; completions counted on the leader's full barrier
-//   warp 1 (leader)     MMA issuer; commits multicast to both CTAs' empty / tfull barriers
-//   warps 2-17          epilogue of this CTA's 128 rows; TMEM release arrives on the leader
-// ------------------------------------------------------------------------------------------
-template <int BN>
-struct Gemm2Cfg {
-  static constexpr int BK = 64;
-  static constexpr int A_BYTES = 128 * BK * 2;
-  static constexpr int B_BYTES = (BN / 2) * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // every byte of smem not needed for epilogue staging goes to the TMA ring: at K = 384 the
-  // MMA otherwise starves on TMA latency (tools/gemm_trace.py)
-  static constexpr int RING = 232448 - 1024 - 256 - EPI_WARPS * STAGE_BUF;
-  static constexpr int STAGES = RING / STAGE_BYTES > 8 ? 8 : RING / STAGE_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + EPI_WARPS * STAGE_BUF + 256;
-};
-
-template <int BN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
-    gemm_pair_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                     const __grid_constant__ CUtensorMap tout, const GemmParams p) {
-  using C = Gemm2Cfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint8_t* sStage = sB + C::STAGES * C::B_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + EPI_WARPS * STAGE_BUF);  // leader's copy used
-  uint64_t* empty = full + C::STAGES;   // both copies used (multicast commit)
-  uint64_t* tfull = empty + C::STAGES;  // [2] both copies used (multicast commit)
-  uint64_t* tempty = tfull + 2;         // [2] leader's copy used (arrivals from both CTAs)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const uint32_t warp = warp_id(), lane = lane_id();
-  const uint32_t rank = cluster_ctarank();
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&ta);
-    tma_prefetch(&tb);
-    if (p.tma_out) tma_prefetch(&tout);
-    for (int i = 0; i < C::STAGES; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 2 * EPI_WARPS);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc2(tslot, C::TMEM_COLS);
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();  // the peer's barriers are initialised before anything can signal them
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  pdl_wait();
-  pdl_trigger();
-  const int ntiles = p.m_tiles * p.n_tiles;  // m_tiles counts 256-row pairs
-  const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int it = 0;
-      for (int t = cid; t < ntiles; t += ncl) {
-        const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
-        const int m0 = mt * 256 + (int)rank * 128, n0 = nt * BN + (int)rank * (BN / 2);
-        for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
-          const int s = it % C::STAGES;
-          mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
-          if (rank == 0) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);
-          tma_load_2d_pair(sA + s * C::A_BYTES, &ta, &full[s], kb * 64, m0);
-          tma_load_2d_pair(sB + s * C::B_BYTES, &tb, &full[s], kb * 64, n0);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (rank == 0 && lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(256, BN);
-      int it = 0, i = 0, tn = 0;
-      for (int t = cid; t < ntiles; t += ncl, ++i) {
-        const int acc = i & 1;
-        GEMM_TRACE(tn, 1);
-        mbar_wait_cluster(&tempty[acc], ((i >> 1) & 1) ^ 1);
-        tc_fence_after();
-        GEMM_TRACE(tn, 2);
-        const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
-          const int s = it % C::STAGES;
-          mbar_wait(&full[s], (it / C::STAGES) & 1);
-          tc_fence_after();
-          GEMM_TRACE(tn, 10 + kb);
-          const uint32_t a0 = smem_u32(sA + s * C::A_BYTES);
-          const uint32_t b0 = smem_u32(sB + s * C::B_BYTES);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_f16_pair(d, smem_desc(a0 + k * 32, 16, 1024, 2), smem_desc(b0 + k * 32, 16, 1024, 2), idesc,
-                          (kb | k) != 0);
-          umma_commit_pair(&empty[s]);
-        }
-        umma_commit_pair(&tfull[acc]);
-      }
-    }
-  } else {
-    const int e = warp - 2;
-    const int q = warp & 3;
-    const int chalf = e >> 2;
-    const int r = q * 32 + lane;
-    uint8_t* stg_base = sStage + e * STAGE_BUF;
-    int nstore = 0;
-    int i = 0;
-    for (int t = cid; t < ntiles; t += ncl, ++i) {
-      const int acc = i & 1;
-      const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
-      const int m0 = mt * 256 + (int)rank * 128, n0 = nt * BN;
-      const int64_t gpix = m0 + r;
-      const bool valid = gpix < p.M;
-      mbar_wait(&tfull[acc], (i >> 1) & 1);
-      tc_fence_after();
-#pragma unroll 1
-      for (int c = chalf; c < BN / 32; c += EPI_SPLIT) {
-        const int c0 = c * 32;
-        float v[32];
-        tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c0, v);
-        tmem_ld_wait();
-        if (c + EPI_SPLIT >= BN / 32) {  // this warp's last TMEM read of the tile
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_leader(&tempty[acc]);
-        }
-        const int col0 = n0 + c0;
-        if (col0 >= p.ep.N) continue;  // warp-uniform
-        if (p.tma_out) {
-          epilogue_tma_chunk(p, &tout, v, col0, m0 + q * 32, stg_base, nstore);
-        } else if (valid) {
-          epilogue_direct(p.ep, gpix, col0, v);
-        }
-      }
-    }
-    if (lane == 0) bulk_wait0();
-  }
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();  // both CTAs are done with TMEM and with each other's barriers
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc2(tmem, C::TMEM_COLS);
-  }
-}
-
-// ------------------------------------------------------------------------------------------
-// GEMM whose A operand is LayerNorm(residual), built by the epilogue warps in the prologue and
-// kept resident in smem for every N tile of the CTA's 128-row block (replaces LN kernel + GEMM
-// for the backbone's LN1 -> QKV and LN2 -> FC1 at D = 384). A: 6 K-blocks of 128 x 64 bf16 in the
-// UMMA SWIZZLE_128B K-major layout, written with st.shared exactly where TMA would have put
-// them; only B streams (32 KB per K-block instead of 48). LN math: ln.cuh (bit-identical to the
-// standalone kernel). One M block per CTA at the engine's M (129 blocks), N tiles in sequence
-// with double-buffered TMEM accumulators.
-// Measured (tools/microbench.py --only ln, graph-timed, M = 16400): QKV 24.3 us vs LN 6.0 + GEMM
-// 18.7; FC1+GELU 35.8 vs 6.2 + 27.3. The prologue (25 MB of residual, ~3.8 us) cannot overlap
-// the MMAs (every row's statistics precede its first K-block) and 129 M blocks leave 19 SMs
-// idle, so the backbone keeps the separate LayerNorm; this path is parity-tested, not used.
-// ------------------------------------------------------------------------------------------
-constexpr int LN_D = 384, LN_KB = LN_D / 64;
-constexpr int LN_BST = 3;     // B stages
-constexpr int LN_STG = 2048;  // per epilogue warp: one 32 x 32 bf16 staging buffer
-
-template <int BN>
-struct GemmLnCfg {
-  static constexpr int A_BYTES = LN_KB * 16384;
-  static constexpr int B_BYTES = BN * 64 * 2;
-  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
-  static constexpr size_t SMEM = 1024 + A_BYTES + (size_t)LN_BST * B_BYTES + EPI_WARPS * LN_STG + 256;
-};
-
-// smem offset of bf16 columns [c, c+4) of A row r (c % 4 == 0) in the SWIZZLE_128B K-major layout
-VPE_DEV uint32_t ln_a_off(int r, int c) {
-  const int kb = c >> 6, j = (c & 63) >> 3;
-  return (uint32_t)(kb * 16384 + (r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4) + ((c >> 2) & 1) * 8);
-}
-
-// epilogue_tma_chunk for bf16 output with a single 2 KB staging buffer per warp
-VPE_DEV void epilogue_tma_chunk1(const GemmParams& p, const CUtensorMap* tout, float (&v)[32], int col0, int row0,
-                                 uint8_t* stg) {
-  const uint32_t lane = lane_id();
-  const int N = p.ep.N;
-  const bool fullc = col0 + 32 <= N;
-  if (p.ep.bias) add_vec32(v, p.ep.bias, col0, N, fullc);
-  if (p.ep.act == ACT_GELU) {
-    gelu_poly32(v);
-  } else if (p.ep.act != ACT_NONE) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], p.ep.act);
-  }
-  if (lane == 0) bulk_wait_read0();  // the previous store from this buffer has read it
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    uint4 u;
-    u.x = pack_bf16(v[8 * k + 0], v[8 * k + 1]);
-    u.y = pack_bf16(v[8 * k + 2], v[8 * k + 3]);
-    u.z = pack_bf16(v[8 * k + 4], v[8 * k + 5]);
-    u.w = pack_bf16(v[8 * k + 6], v[8 * k + 7]);
-    *reinterpret_cast<uint4*>(stg + lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4)) = u;
-  }
-  fence_async_smem();
-  __syncwarp();
-  if (lane == 0) {
-    tma_store_2d(tout, stg, col0, row0);
-    bulk_commit();
-  }
-}
-
-template <int BN>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    gemm_ln_kernel(const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap tout,
-                   const GemmParams p) {
-  using C = GemmLnCfg<BN>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = sA + C::A_BYTES;
-  uint8_t* sStg = sB + LN_BST * C::B_BYTES;
-  uint64_t* b_full = reinterpret_cast<uint64_t*>(sStg + EPI_WARPS * LN_STG);
-  uint64_t* b_empty = b_full + LN_BST;
-  uint64_t* tfull = b_empty + LN_BST;  // [2]
-  uint64_t* tempty = tfull + 2;        // [2]
-  uint64_t* a_full = tempty + 2;
-  uint64_t* a_empty = a_full + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(a_empty + 1);
-
-  const uint32_t warp = warp_id(), lane = lane_id();
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tb);
-    tma_prefetch(&tout);
-    for (int i = 0; i < LN_BST; ++i) {
-      mbar_init(&b_full[i], 1);
-      mbar_init(&b_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPI_WARPS);
-    }
-    mbar_init(a_full, EPI_WARPS);
-    mbar_init(a_empty, 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  pdl_wait();
-  pdl_trigger();
-  const int n_tiles = p.n_tiles, m_tiles = p.m_tiles;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x)
-        for (int nt = 0; nt < n_tiles; ++nt)
-          for (int kb = 0; kb < LN_KB; ++kb) {
-            mbar_wait(&b_empty[s], ph ^ 1);
-            mbar_expect_tx(&b_full[s], C::B_BYTES);
-            tma_load_2d(sB + s * C::B_BYTES, &tb, &b_full[s], kb * 64, nt * BN);
-            if (++s == LN_BST) {
-              s = 0;
-              ph ^= 1;
-            }
-          }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(128, BN);
-      const uint64_t a_desc0 = smem_desc(smem_u32(sA), 16, 1024, 2);
-      const uint64_t b_desc0 = smem_desc(smem_u32(sB), 16, 1024, 2);
-      const uint32_t a_hi = (uint32_t)(a_desc0 >> 32), b_hi = (uint32_t)(b_desc0 >> 32);
-      int s = 0, i = 0, mi = 0;
-      uint32_t ph = 0;
-      for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x, ++mi) {
-        mbar_wait(a_full, mi & 1);  // this block's LN(x) is in smem
-        tc_fence_after();
-        for (int nt = 0; nt < n_tiles; ++nt, ++i) {
-          const int acc = i & 1;
-          mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t d = tmem + acc * BN;
-#pragma unroll 1
-          for (int kb = 0; kb < LN_KB; ++kb) {
-            mbar_wait(&b_full[s], ph);
-            tc_fence_after();
-            const uint32_t a_lo = (uint32_t)a_desc0 + (uint32_t)kb * (16384 >> 4);
-            const uint32_t b_lo = (uint32_t)b_desc0 + (uint32_t)s * (C::B_BYTES >> 4);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              umma_f16(d, ((uint64_t)a_hi << 32) | (a_lo + 2 * k), ((uint64_t)b_hi << 32) | (b_lo + 2 * k), idesc,
-                       (kb | k) != 0);
-            umma_commit(&b_empty[s]);
-            if (++s == LN_BST) {
-              s = 0;
-              ph ^= 1;
-            }
-          }
-          umma_commit(&tfull[acc]);
-        }
-        umma_commit(a_empty);  // every MMA reading this block's A has completed
-      }
-    }
-  } else {
-    const int e = warp - 2;
-    const int q = warp & 3;
-    const int chalf = e >> 2;
-    uint8_t* stg = sStg + e * LN_STG;
-    int i = 0, mi = 0;
-    for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x, ++mi) {
-      // prologue: rows e, e + 16, ... of the block -> LN -> bf16 A in smem (+ the tap LN)
-      mbar_wait(a_empty, (mi & 1) ^ 1);  // the previous block's MMAs are done with A
-#pragma unroll 1
-      for (int rl = e; rl < 128; rl += EPI_WARPS) {
-        const int64_t row = (int64_t)mt * 128 + rl;
-        if (row < p.M) {
-          float4 v[LN_D / 128];
-          ln_load<LN_D / 128>(p.ln.x, row, LN_D, lane, v);
-          float mean, rstd;
-          ln_stats<LN_D / 128>(v, LN_D, p.ln.eps, mean, rstd);
-#pragma unroll
-          for (int k = 0; k < LN_D / 128; ++k) {
-            const int c = (k * 32 + lane) * 4;
-            *reinterpret_cast<uint2*>(sA + ln_a_off(rl, c)) = ln_affine4(v[k], mean, rstd, p.ln.w, p.ln.b, c);
-            if (p.ln.tap)
-              *reinterpret_cast<uint2*>(p.ln.tap + row * LN_D + c) = ln_affine4(v[k], mean, rstd, p.ln.tw, p.ln.tb, c);
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < LN_D / 128; ++k)
-            *reinterpret_cast<uint2*>(sA + ln_a_off(rl, (k * 32 + lane) * 4)) = make_uint2(0u, 0u);
-        }
-      }
-      fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-      __syncwarp();
-      if (lane == 0) mbar_arrive(a_full);
-      for (int nt = 0; nt < n_tiles; ++nt, ++i) {
-        const int acc = i & 1;
-        mbar_wait(&tfull[acc], (i >> 1) & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = chalf; c < BN / 32; c += EPI_SPLIT) {
-          float v[32];
-          tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c * 32, v);
-          tmem_ld_wait();
-          if (c + EPI_SPLIT >= BN / 32) {  // this warp's last TMEM read of the tile
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
-          const int col0 = nt * BN + c * 32;
-          if (col0 >= p.ep.N) continue;  // warp-uniform
-          epilogue_tma_chunk1(p, &tout, v, col0, mt * 128 + q * 32, stg);
         }
       }
     }
@@ -1576,78 +1209,8 @@ static void finish_grid(GemmPlan* g, int N, int bn, int m_tiles) {
   g->grid = dim3(ctas, 1, 1);
 }
 
-template <typename K>
-static int max_pair_clusters(K kernel, int smem) {
-  static int cached[4] = {0, 0, 0, 0};
-  const int slot = smem % 4;  // distinct per instantiation in practice; recomputed if 0
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * 256, 1, 1);
-  cfg.blockDim = dim3(GEMM_THREADS, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = 2;
-  attr.val.clusterDim.y = 1;
-  attr.val.clusterDim.z = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
-    cudaGetLastError();
-    n = num_sms() / 2;
-  }
-  (void)cached;
-  (void)slot;
-  static bool printed = false;
-  if (!printed && getenv("VPE_VERBOSE")) {
-    fprintf(stderr, "[vpe] pair GEMM: %d co-resident clusters of 2 (smem %d)\n", n, smem);
-    printed = true;
-  }
-  return n;
-}
-
-static int plan_gemm_rows_pair(GemmPlan* g, const __nv_bfloat16* A, int M, int K, int64_t lda, const __nv_bfloat16* B,
-                               int N, int Kb, int64_t ldb, const EpiParams& ep, int bn) {
-  if (bn != 128 && bn != 192 && bn != 256) return VPE_E_SHAPE;
-  if (K % 64 || Kb != K) return VPE_E_SHAPE;
-  if ((lda * 2) % 16 || (reinterpret_cast<uintptr_t>(A) % 16)) return VPE_E_SHAPE;
-  memset(g, 0, sizeof(*g));
-  uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
-  uint64_t strides[1] = {(uint64_t)lda * 2};
-  uint32_t box[2] = {64u, 128u};
-  VPE_TRY(encode_tma(&g->ta, 2, A, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B));
-  VPE_TRY(make_b_map(g, B, N, Kb, ldb, bn / 2, 64));
-  g->p.kblocks = Kb / 64;
-  g->p.kblocks_a = K / 64;
-  g->p.mode = 0;
-  g->p.M = M;
-  g->p.ks = 1;
-  g->p.cchunks = 1;
-  g->p.ep = ep;
-  VPE_TRY(make_out_map(g, M));
-  g->p.n_tiles = (N + bn - 1) / bn;
-  g->p.m_tiles = (M + 255) / 256;
-  const int tiles = g->p.n_tiles * g->p.m_tiles;
-  g->bn = bn;
-  g->bk = 64;
-  g->pair = 1;
-  int pairs = 0;
-#define VPE_P2(BN_)                              \
-  if (bn == BN_) {                               \
-    g->smem = Gemm2Cfg<BN_>::SMEM;               \
-    pairs = max_pair_clusters(gemm_pair_kernel<BN_>, (int)g->smem); \
-  }
-  VPE_P2(128) VPE_P2(192) VPE_P2(256)
-#undef VPE_P2
-  // persistent grid = the clusters that can be co-resident (TPCs with both SMs enabled), not #SMs/2
-  g->grid = dim3(2 * (tiles < pairs ? tiles : pairs), 1, 1);
-  return VPE_OK;
-}
-
 int plan_gemm_rows(GemmPlan* g, const __nv_bfloat16* A, int M, int K, int64_t lda, const __nv_bfloat16* B, int N,
                    int Kb, int64_t ldb, const EpiParams& ep, int bn) {
-  if (bn < 0) return plan_gemm_rows_pair(g, A, M, K, lda, B, N, Kb, ldb, ep, -bn);
   const int bk = 64;
   if (K % bk || Kb % K || smem_for(bn, bk) < 0) return VPE_E_SHAPE;
   if ((lda * 2) % 16 || (reinterpret_cast<uintptr_t>(A) % 16)) return VPE_E_SHAPE;
@@ -1751,19 +1314,13 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   if ((pitch_px * 2) % 16 || (pitch_row * 2) % 16 || (pitch_img * 2) % 16 || reinterpret_cast<uintptr_t>(X) % 16)
     return VPE_E_SHAPE;
   memset(g, 0, sizeof(*g));
-  if (true) {
+  {
     // 4D view {ch, x, y, img}, box {8 kc, P, rows, 1}, SWIZZLE_128B / 64B: one row per pixel
     uint64_t dims[4] = {(uint64_t)Cp, (uint64_t)W, (uint64_t)H, (uint64_t)nimg};
     uint64_t strides[3] = {(uint64_t)pitch_px * 2, (uint64_t)pitch_row * 2, (uint64_t)pitch_img * 2};
     uint32_t box[4] = {8u * kc, (uint32_t)P, (uint32_t)rows_box, 1u};
     VPE_TRY(encode_tma(&g->ta, 4, X, dims, strides, box,
                        kc == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B));
-  } else {
-    // 5D view {8 ch, x, y, chunk, img}: TMA writes [chunk][y][x][8ch] = the no-swizzle K-major layout
-    uint64_t dims[5] = {8, (uint64_t)W, (uint64_t)H, (uint64_t)(Cp / 8), (uint64_t)nimg};
-    uint64_t strides[4] = {(uint64_t)pitch_px * 2, (uint64_t)pitch_row * 2, 16, (uint64_t)pitch_img * 2};
-    uint32_t box[5] = {8u, (uint32_t)P, (uint32_t)rows_box, (uint32_t)kc, 1u};
-    VPE_TRY(encode_tma(&g->ta, 5, X, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE));
   }
   const int gch = 8 * kc;
   VPE_TRY(make_b_map(g, B, N, parts * 9 * Cp, ldb, bn, gch));
@@ -1810,11 +1367,10 @@ static int launch_halo_t(const GemmPlan& g0, cudaStream_t s) {
     g_gemm_trace_on = (e && e[0] == '1') ? 1 : 0;
   }
   g.p.trace = g_gemm_trace_on;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static OncePerDevice attr_set;
+  if (attr_set.first()) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HaloCfg<BN, KC, RT, WRES>::SMEM);
     max_smem_carveout(k);
-    attr_set = true;
   }
   PdlKind pk(8);
   return launch_k(k, g.grid, dim3(GEMM_THREADS), HaloCfg<BN, KC, RT, WRES>::SMEM, s, g.ta, g.tb, g.p) == cudaSuccess
@@ -1825,11 +1381,10 @@ static int launch_halo_t(const GemmPlan& g0, cudaStream_t s) {
 template <int BN, int BK>
 static int launch_t(const GemmPlan& g, cudaStream_t s) {
   auto k = gemm_tc_kernel<BN, BK>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static OncePerDevice attr_set;
+  if (attr_set.first()) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GemmCfg<BN, BK>::SMEM);
     max_smem_carveout(k);
-    attr_set = true;
   }
   if (g_gemm_trace_on < 0) {
     const char* e = getenv("VPE_GEMM_TRACE");
@@ -1839,68 +1394,6 @@ static int launch_t(const GemmPlan& g, cudaStream_t s) {
   p.trace = g_gemm_trace_on;
   PdlKind pk(1);
   return launch_k(k, g.grid, dim3(GEMM_THREADS), GemmCfg<BN, BK>::SMEM, s, g.ta, g.tb, g.tout, p) == cudaSuccess
-             ? VPE_OK
-             : VPE_E_CUDA;
-}
-
-template <int BN>
-static int launch_pair_t(const GemmPlan& g, cudaStream_t s) {
-  auto k = gemm_pair_kernel<BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Gemm2Cfg<BN>::SMEM);
-    attr_set = true;
-  }
-  if (g_gemm_trace_on < 0) {
-    const char* e = getenv("VPE_GEMM_TRACE");
-    g_gemm_trace_on = (e && e[0] == '1') ? 1 : 0;
-  }
-  GemmParams p = g.p;
-  p.trace = g_gemm_trace_on;
-  k<<<g.grid, GEMM_THREADS, Gemm2Cfg<BN>::SMEM, s>>>(g.ta, g.tb, g.tout, p);
-  return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
-}
-
-int plan_gemm_ln(GemmPlan* g, const float* x, int M, int D, const float* w, const float* b, float eps,
-                 const float* tw, const float* tb, const __nv_bfloat16* B, int N, const EpiParams& ep, int bn) {
-  if (D != LN_D || bn != 256 || ep.kind != EPI_BF16 || !x || !w || !b) return VPE_E_SHAPE;
-  if (reinterpret_cast<uintptr_t>(x) % 16) return VPE_E_SHAPE;
-  memset(g, 0, sizeof(*g));
-  VPE_TRY(make_b_map(g, B, N, D, D, bn, 64));
-  g->p.ep = ep;
-  g->p.M = M;
-  VPE_TRY(make_out_map(g, M));
-  if (!g->p.tma_out) return VPE_E_SHAPE;
-  g->p.kblocks = D / 64;
-  g->p.n_tiles = (N + bn - 1) / bn;
-  g->p.m_tiles = (M + 127) / 128;
-  g->p.ln.x = x;
-  g->p.ln.w = w;
-  g->p.ln.b = b;
-  g->p.ln.eps = eps;
-  g->p.ln.tw = tw;
-  g->p.ln.tb = tb;
-  g->grid = dim3(g->p.m_tiles < num_sms() ? g->p.m_tiles : num_sms(), 1, 1);
-  g->bn = bn;
-  g->bk = 64;
-  g->ln = 1;
-  g->smem = GemmLnCfg<256>::SMEM;
-  return VPE_OK;
-}
-
-int launch_gemm_ln(const GemmPlan& g0, __nv_bfloat16* tap, cudaStream_t s) {
-  if (!g0.ln || g0.bn != 256) return VPE_E_SHAPE;
-  if (tap && (!g0.p.ln.tw || !g0.p.ln.tb)) return VPE_E_VALUE;
-  GemmPlan g = g0;
-  g.p.ln.tap = tap;
-  auto k = gemm_ln_kernel<256>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GemmLnCfg<256>::SMEM);
-    attr_set = true;
-  }
-  PdlKind pk(1);
-  return launch_k(k, g.grid, dim3(GEMM_THREADS), GemmLnCfg<256>::SMEM, s, g.tb, g.tout, g.p) == cudaSuccess
              ? VPE_OK
              : VPE_E_CUDA;
 }
@@ -1967,11 +1460,10 @@ int launch_gemm_resid_ln(const GemmPlan& g0, __nv_bfloat16* xln, __nv_bfloat16* 
     if (!g.p.ln.tw || !g.p.ln.tb) return VPE_E_VALUE;
     VPE_TRY(bf16_rows_map(&ttap, tap, g.p.M, RL_N));
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  static OncePerDevice attr_set;
+  if (attr_set.first()) {
     cudaFuncSetAttribute(gemm_resid_ln_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RlCfg::SMEM);
     max_smem_carveout(gemm_resid_ln_kernel);
-    attr_set = true;
   }
   PdlKind pk(1);
   return launch_k(gemm_resid_ln_kernel, g.grid, dim3(RL_THREADS), RlCfg::SMEM, s, g.ta, g.tb, g.tout, g.tx, ttap,
@@ -1982,13 +1474,6 @@ int launch_gemm_resid_ln(const GemmPlan& g0, __nv_bfloat16* xln, __nv_bfloat16* 
 
 int launch_gemm(const GemmPlan& g, cudaStream_t s) {
   if (g.resid_ln) return launch_gemm_resid_ln(g, nullptr, nullptr, s);
-  if (g.ln) return launch_gemm_ln(g, nullptr, s);
-  if (g.pair) {
-    if (g.bn == 128) return launch_pair_t<128>(g, s);
-    if (g.bn == 192) return launch_pair_t<192>(g, s);
-    if (g.bn == 256) return launch_pair_t<256>(g, s);
-    return VPE_E_SHAPE;
-  }
   if (g.halo_kc) {
 #define VPE_LH(BN_, KC_, RT_)                                                         \
   if (g.bn == BN_ && g.halo_kc == KC_ && g.halo_rt == RT_)                            \

@@ -46,7 +46,7 @@ struct EpiParams {
   float* depth = nullptr;
 };
 
-// LayerNorm computed in the GEMM prologue (gemm_ln_kernel): A = LN(x) over D = K columns
+// LayerNorm fused into the residual GEMM's epilogue (gemm_resid_ln_kernel)
 struct LnParams {
   const float* x = nullptr;  // fp32 residual stream [M, D]
   const float* w = nullptr;
@@ -85,8 +85,6 @@ struct GemmPlan {
   int halo_kc = 0;  // > 0: conv_halo_kernel<bn, halo_kc, halo_rt>
   int halo_rt = 1;
   int halo_wres = 0;  // 1: conv_halo_kernel<.., WRES> (all weight tiles resident in smem)
-  int pair = 0;     // 1: gemm_pair_kernel<bn> (cta_group::2, 256-row tiles)
-  int ln = 0;       // 1: gemm_ln_kernel<bn> (A = LayerNorm(p.ln.x) built in the prologue)
   int resid_ln = 0; // 1: gemm_resid_ln_kernel (residual GEMM + the next LayerNorm in the epilogue)
   CUtensorMap tx;   // resid_ln: bf16 LayerNorm output map
   size_t smem = 0;
@@ -104,7 +102,6 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
 bool tma_available();
 // Row-major A [M, K] (pitch lda elements) times K-major weights B [N, Kb] (pitch ldb).
 // Kb may be a multiple of K (split-precision weights concatenated along K; A repeats).
-// bn < 0 selects the CTA-pair kernel with 256 x |bn| tiles (|bn| in {128, 192, 256}, Kb == K).
 int plan_gemm_rows(GemmPlan* g, const __nv_bfloat16* A, int M, int K, int64_t lda,
                    const __nv_bfloat16* B, int N, int Kb, int64_t ldb, const EpiParams& ep, int bn);
 // NHWC image X (channels C real, pitches in elements: pixel, row, image) as implicit-GEMM conv
@@ -113,12 +110,6 @@ int plan_gemm_conv(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
                    int64_t pitch_px, int64_t pitch_row, int64_t pitch_img, int ks, int bk,
                    const __nv_bfloat16* B, int N, int Kb, int64_t ldb, const EpiParams& ep, int bn);
 int launch_gemm(const GemmPlan& g, cudaStream_t stream);
-// A = LayerNorm(x) (x fp32 [M, D], D = 384) computed by the GEMM itself and kept resident in smem
-// for all N tiles of its 128-row block; B [N, D] K-major; EPI_BF16 output (bias, optional GELU).
-// The optional tap LN (second affine) is written to `tap` at launch (launch_gemm_ln).
-int plan_gemm_ln(GemmPlan* g, const float* x, int M, int D, const float* w, const float* b, float eps,
-                 const float* tw, const float* tb, const __nv_bfloat16* B, int N, const EpiParams& ep, int bn);
-int launch_gemm_ln(const GemmPlan& g, __nv_bfloat16* tap, cudaStream_t stream);
 // resid [M, 384] fp32 += ls * (A W^T + bias) (A bf16 [M, K], W [384, K]); then xln = LN(resid)
 // with (ln_w, ln_b) in bf16 and optionally tap = LN(resid) with (tw, tb). xln / tap pointers may
 // be given at launch (ring slots); a null xln at plan and launch skips that output.

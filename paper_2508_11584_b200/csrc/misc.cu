@@ -104,17 +104,15 @@ int launch_patch_im2col(const uint8_t* px, __nv_bfloat16* A, int B, int R, int K
                         const float* cls_pos0, int D, cudaStream_t s) {
   const int np = (R / 14) * (R / 14);
   PdlKind pk(16);
-  static bool co = false;
-  if (!co) {
+  static OncePerDevice co;
+  if (co.first()) {
     max_smem_carveout(patch_im2col_kernel);
-    co = true;
   }
   const char* generic = getenv("VPE_IM2COL_GENERIC");  // parity test hook
   if ((R / 14) % IM_PPB == 0 && R % 4 == 0 && KP % 2 == 0 && !(generic && generic[0] == '1')) {
-    static bool co8 = false;
-    if (!co8) {
+    static OncePerDevice co8;
+    if (co8.first()) {
       max_smem_carveout(patch_im2col8_kernel);
-      co8 = true;
     }
     return launch_k(patch_im2col8_kernel, dim3(B * np / IM_PPB + B), dim3(256), 0, s, px, A, B, R, KP, resid,
                     cls_pos0, D) == cudaSuccess
@@ -219,10 +217,9 @@ int launch_layernorm(const float* x, int M, int D, const float* w, const float* 
   switch (D / 128) {
 #define VPE_LN(NV_) \
   case NV_: {                                                                                       \
-    static bool co = false;                                                                          \
-    if (!co) {                                                                                       \
+    static OncePerDevice co;                                                                          \
+    if (co.first()) {                                                                                       \
       max_smem_carveout(layernorm_kernel<NV_>);                                                      \
-      co = true;                                                                                     \
     }                                                                                                \
   }                                                                                                  \
     if (launch_k(layernorm_kernel<NV_>, grid, block, 0, s, x, M, D, w, b, eps, out, w2, b2, out2) != cudaSuccess) \
@@ -368,11 +365,10 @@ int launch_bilinear_ac(const __nv_bfloat16* in, int B, int Hi, int Wi, int cp, _
   static const int mode = getenv("VPE_BILINEAR_GATHER") ? 2 : 0;
   const size_t rows_smem = 2 * row_bytes;
   if (rows_smem <= 96 * 1024 && mode != 2) {
-    static bool attr = false;
-    if (!attr) {
+    static OncePerDevice attr;
+    if (attr.first()) {
       cudaFuncSetAttribute(bilinear_ac_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
       max_smem_carveout(bilinear_ac_rows_kernel);
-      attr = true;
     }
     bilinear_ac_rows_kernel<<<dim3(Ho, B), 256, rows_smem, s>>>(in, Hi, Wi, cp, out, Ho, Wo, C);
     return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;
@@ -416,10 +412,9 @@ int launch_im2col_s2(const __nv_bfloat16* x, int B, int H, int W, int C, __nv_bf
   const int Ho = (H + 1) / 2, Wo = (W + 1) / 2;
   const int64_t total = (int64_t)B * Ho * Wo * 9 * (C / 8);
   if (total >= ((int64_t)1 << 31)) return VPE_E_SHAPE;
-  static bool co = false;
-  if (!co) {
+  static OncePerDevice co;
+  if (co.first()) {
     max_smem_carveout(im2col_s2_kernel);
-    co = true;
   }
   im2col_s2_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(x, B, H, W, C, out, Ho, Wo);
   return cudaGetLastError() == cudaSuccess ? VPE_OK : VPE_E_CUDA;

@@ -481,7 +481,8 @@ int vpe_ring_acquire_latest(vpe_ring* r, uint32_t cid, void* stream, vpe_lease* 
         lease->frame_id = ld64(r->fid(best));
         lease->capture_ts = ld64(r->ts(best));
         lease->consumed = 0;
-        if (stream && r->device != VPE_HOST_PLAIN)
+        // NULL is the legacy default stream, a valid consumer stream: always order it (RAW)
+        if (r->device != VPE_HOST_PLAIN)
           VPE_CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), r->ready[best], 0));
         return VPE_OK;
       }
@@ -503,7 +504,7 @@ static int finish(vpe_ring* r, vpe_lease* lease, void* stream) {
   const int cidx = r->cursor_idx(lease->consumer_id);
   if (cidx < 0) return VPE_E_NOT_FOUND;
   const int k = lease->slot * VPE_MAX_CONSUMERS + cidx;
-  if (stream && r->device != VPE_HOST_PLAIN) {
+  if (r->device != VPE_HOST_PLAIN) {  // NULL = legacy default stream, still recorded (WAR)
     VPE_CUDA_TRY(cudaEventRecord(r->done[k], static_cast<cudaStream_t>(stream)));
     __atomic_store_n(&r->done_valid[k], (uint8_t)1, __ATOMIC_RELEASE);
   }
@@ -541,7 +542,7 @@ int vpe_ring_consume(vpe_ring* r, vpe_lease* lease, const int32_t* labels, int32
 int vpe_ring_release(vpe_ring* r, vpe_lease* lease, void* stream) {
   if (!r || !lease) return VPE_E_VALUE;
   if (lease->consumed) return VPE_OK;  // channels.py:478-479
-  if (stream && r->device != VPE_HOST_PLAIN) {
+  if (r->device != VPE_HOST_PLAIN) {
     const int cidx = r->cursor_idx(lease->consumer_id);
     if (cidx >= 0) {
       const int k = lease->slot * VPE_MAX_CONSUMERS + cidx;
@@ -555,7 +556,7 @@ int vpe_ring_release(vpe_ring* r, vpe_lease* lease, void* stream) {
 }
 
 // channels.py:377-421
-int vpe_ring_pop(vpe_ring* r, uint32_t cid, void* const* dst, void* stream, vpe_lease* env) {
+int vpe_ring_pop(vpe_ring* r, uint32_t cid, void* const* dst, int32_t dst_on_host, void* stream, vpe_lease* env) {
   if (!r) return VPE_E_VALUE;
   if (r->mode != VPE_FIFO) return VPE_E_CONFIG;
   const int cidx = r->cursor_idx(cid);
@@ -575,7 +576,7 @@ int vpe_ring_pop(vpe_ring* r, uint32_t cid, void* const* dst, void* stream, vpe_
     if (cas32(r->state(best), STATE_READY, STATE_READY + 1) != STATE_READY) continue;
     const uint64_t fid = ld64(r->fid(best));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (st && r->device != VPE_HOST_PLAIN) {
+    if (!dst_on_host && r->device != VPE_HOST_PLAIN) {
       VPE_CUDA_TRY(cudaStreamWaitEvent(st, r->ready[best], 0));
       for (int l = 0; l < r->nspecs; ++l) {
         VPE_CUDA_TRY(cudaMemcpyAsync(dst[l], r->slot_ptr(best, l), r->nbytes[l], cudaMemcpyDefault, st));
@@ -583,7 +584,7 @@ int vpe_ring_pop(vpe_ring* r, uint32_t cid, void* const* dst, void* stream, vpe_
       }
       const int k = best * VPE_MAX_CONSUMERS + cidx;
       VPE_CUDA_TRY(cudaEventRecord(r->done[k], st));
-      r->done_valid[k] = 1;
+      __atomic_store_n(&r->done_valid[k], (uint8_t)1, __ATOMIC_RELEASE);
     } else {
       // host consumer: wait for the producer's writes, then copy on the host
       if (r->device != VPE_HOST_PLAIN) VPE_CUDA_TRY(cudaEventSynchronize(r->ready[best]));
@@ -686,10 +687,12 @@ int shm_map(const char* name, size_t bytes, bool create, void** base, size_t* ma
   *mapped = bytes;
   return VPE_OK;
 }
+// segment names follow the reference's "<namespace>.<region>" convention (arena.py:163-165,
+// channels.py:568 "<name>-c"), so shm_census / clean_namespace see them
 void shm_names(vpe_ring* r, const char* name) {
-  snprintf(r->nm_hdr, sizeof(r->nm_hdr), "/vpe.%s-c", name);
-  snprintf(r->nm_ipc, sizeof(r->nm_ipc), "/vpe.%s-x", name);
-  snprintf(r->nm_dat, sizeof(r->nm_dat), "/vpe.%s-d", name);
+  snprintf(r->nm_hdr, sizeof(r->nm_hdr), "/%s-c", name);
+  snprintf(r->nm_ipc, sizeof(r->nm_ipc), "/%s-x", name);
+  snprintf(r->nm_dat, sizeof(r->nm_dat), "/%s-d", name);
 }
 }  // namespace
 
@@ -876,6 +879,150 @@ int vpe_ring_attach(const char* name, vpe_ring** out) {
       return VPE_E_CUDA;
     }
   *out = r;
+  return VPE_OK;
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// Shareable regions: the reference's create_region / attach_region (arena.py:285-313) with the
+// bytes in HBM (CUDA IPC export) or in POSIX shared memory (VPE_HOST_PLAIN). A POSIX segment
+// "/<namespace>.<region>" always exists for a region: for a host region it holds the bytes, for
+// a device region a descriptor {magic, device, bytes, cudaIpcMemHandle}.
+struct vpe_region {
+  int32_t device = 0;
+  int role = 0;  // 1 creator, 2 attached
+  size_t bytes = 0;
+  uint8_t* base = nullptr;
+  void* seg = nullptr;
+  size_t seg_bytes = 0;
+  char nm[192] = {0};
+};
+namespace {
+constexpr char REG_MAGIC[8] = {'P', 'E', 'R', 'E', 'G', '1', 0, 0};
+struct RegDesc {
+  char magic[8];
+  int32_t device, pad;
+  uint64_t bytes;
+  cudaIpcMemHandle_t mem;
+};
+bool region_name_ok(const char* name) {
+  return name && name[0] && strlen(name) <= 150 && !strchr(name, '/');
+}
+}  // namespace
+
+int vpe_region_destroy(vpe_region* g, int32_t unlink) {
+  if (!g) return VPE_OK;
+  if (g->device >= 0 && g->base) {
+    if (g->role == 2)
+      cudaIpcCloseMemHandle(g->base);
+    else
+      cudaFree(g->base);
+  }
+  if (g->seg) munmap(g->seg, g->seg_bytes);
+  if (unlink && g->nm[0]) shm_unlink(g->nm);
+  delete g;
+  return VPE_OK;
+}
+
+int vpe_region_create(const char* name, uint64_t nbytes, int32_t device, vpe_region** out) {
+  if (!out || !region_name_ok(name) || nbytes == 0) return VPE_E_CONFIG;
+  if (device == VPE_HOST_PINNED) return VPE_E_CONFIG;  // pinned host memory is not shareable here
+  vpe_region* g = new (std::nothrow) vpe_region();
+  if (!g) return VPE_E_RESOURCE;
+  snprintf(g->nm, sizeof(g->nm), "/%s", name);
+  g->device = device;
+  g->bytes = nbytes;
+  g->role = 1;
+  const bool host = device == VPE_HOST_PLAIN;
+  int rc = shm_map(g->nm, host ? nbytes : sizeof(RegDesc), true, &g->seg, &g->seg_bytes);
+  if (rc) {
+    g->nm[0] = 0;  // never unlink a segment we did not create (AlreadyExists)
+    vpe_region_destroy(g, 0);
+    return rc;
+  }
+  memset(g->seg, 0, g->seg_bytes);  // zero-initialised
+  if (host) {
+    g->base = static_cast<uint8_t*>(g->seg);
+    *out = g;
+    return VPE_OK;
+  }
+  RegDesc* d = static_cast<RegDesc*>(g->seg);
+  if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(reinterpret_cast<void**>(&g->base), nbytes) != cudaSuccess ||
+      cudaMemset(g->base, 0, nbytes) != cudaSuccess || cudaIpcGetMemHandle(&d->mem, g->base) != cudaSuccess) {
+    cudaGetLastError();
+    vpe_region_destroy(g, 1);
+    return VPE_E_RESOURCE;
+  }
+  d->device = device;
+  d->bytes = nbytes;
+  memcpy(d->magic, REG_MAGIC, 8);  // published last: attachers see a complete descriptor
+  *out = g;
+  return VPE_OK;
+}
+
+int vpe_region_attach(const char* name, uint64_t expect_bytes, vpe_region** out) {
+  if (!out || !region_name_ok(name)) return VPE_E_CONFIG;
+  vpe_region* g = new (std::nothrow) vpe_region();
+  if (!g) return VPE_E_RESOURCE;
+  snprintf(g->nm, sizeof(g->nm), "/%s", name);
+  g->role = 2;
+  const int rc = shm_map(g->nm, 0, false, &g->seg, &g->seg_bytes);
+  if (rc) {
+    g->nm[0] = 0;
+    vpe_region_destroy(g, 0);
+    return rc;
+  }
+  const RegDesc* d = static_cast<const RegDesc*>(g->seg);
+  const bool dev = g->seg_bytes >= sizeof(RegDesc) && memcmp(d->magic, REG_MAGIC, 8) == 0;
+  if (!dev) {  // a host region: the segment is the bytes
+    g->device = VPE_HOST_PLAIN;
+    g->bytes = g->seg_bytes;
+    g->base = static_cast<uint8_t*>(g->seg);
+  } else {
+    g->device = d->device;
+    g->bytes = d->bytes;
+    void* p = nullptr;
+    if (cudaSetDevice(d->device) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&p, d->mem, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      g->nm[0] = 0;
+      vpe_region_destroy(g, 0);
+      return VPE_E_RESOURCE;
+    }
+    g->base = static_cast<uint8_t*>(p);
+  }
+  if (g->bytes < expect_bytes) {  // attach_region: handle larger than the mapping (arena.py:310-312)
+    g->nm[0] = 0;
+    vpe_region_destroy(g, 0);
+    return VPE_E_CORRUPT_HANDLE;
+  }
+  *out = g;
+  return VPE_OK;
+}
+
+int vpe_region_info(vpe_region* g, void** base, uint64_t* bytes, int32_t* device) {
+  if (!g) return VPE_E_VALUE;
+  if (base) *base = g->base;
+  if (bytes) *bytes = g->bytes;
+  if (device) *device = g->device;
+  return VPE_OK;
+}
+
+// copy_out (arena.py:367-373): the single permitted copy, stream-ordered for device memory;
+// host_sync != 0 returns only when the bytes are in dst
+int vpe_copy_out(void* dst, const void* src, uint64_t nbytes, void* stream, int32_t host_sync) {
+  if ((!dst || !src) && nbytes) return VPE_E_VALUE;
+  cudaPointerAttributes a{}, b{};
+  const bool dev_src = cudaPointerGetAttributes(&a, src) == cudaSuccess && a.type == cudaMemoryTypeDevice;
+  const bool dev_dst = cudaPointerGetAttributes(&b, dst) == cudaSuccess && b.type == cudaMemoryTypeDevice;
+  cudaGetLastError();
+  if (!dev_src && !dev_dst) {
+    memcpy(dst, src, nbytes);
+  } else {
+    VPE_CUDA_TRY(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+    if (host_sync) VPE_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  }
+  g_copies.fetch_add(1);
   return VPE_OK;
 }
 

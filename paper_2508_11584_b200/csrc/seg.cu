@@ -181,12 +181,11 @@ int launch_upsample_argmax(const float* logits, int B, int h, int C, int cp, int
   const size_t smem = (size_t)2 * h * ((C + 1) & ~1) * sizeof(float);
   if (B < 1 || h < 1 || C < 1 || C > 256 || cp < C || R > 1024 || R != 14 * h || smem > 227 * 1024)
     return VPE_E_CONFIG;
-  static bool attr = false;
-  if (!attr) {
+  static OncePerDevice attr;
+  if (attr.first()) {
     VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       227 * 1024));
     max_smem_carveout(seg_upsample_argmax_kernel);
-    attr = true;
   }
   seg_upsample_argmax_kernel<<<dim3(2 * h, B), (R + 31) / 32 * 32, smem, st>>>(logits, h, C, cp, R, labels, 0.f);
   VPE_CUDA_TRY(cudaGetLastError());

@@ -1,5 +1,6 @@
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <utility>
@@ -23,6 +24,17 @@
   } while (0)
 
 namespace vpe {
+// "first call on the current device": kernel attributes (max dynamic smem, carveout) are set per
+// device, so a process driving several GPUs must set them once on each of them
+struct OncePerDevice {
+  std::atomic<uint64_t> done{0};
+  bool first() {
+    int d = 0;
+    cudaGetDevice(&d);
+    const uint64_t bit = 1ull << (d & 63);
+    return !(done.fetch_or(bit, std::memory_order_acq_rel) & bit);
+  }
+};
 // Programmatic dependent launch: a process-wide switch set per engine before it captures its
 // graphs (vpe_set_pdl; VPE_PDL=0/1 overrides). Measured: latency mode (batch 1) backbone 0.752 ->
 // 0.695 ms and head p50 -8..-9%; throughput mode with concurrent head streams 3.51 -> 3.57 ms

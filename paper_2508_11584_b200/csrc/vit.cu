@@ -12,7 +12,6 @@
 #include "attention.cuh"
 #include "gemm.cuh"
 #include "misc.cuh"
-#include "mlp.cuh"
 #include "runtime.h"
 #include "util.cuh"
 
@@ -27,8 +26,6 @@ struct vpe_vit {
   GemmPlan patch;
   GemmPlan qkv_g[VPE_MAX_LAYERS], proj_g[VPE_MAX_LAYERS], fc1_g[VPE_MAX_LAYERS], fc2_g[VPE_MAX_LAYERS];
   AttnPlan attn;
-  MlpPlan mlp[VPE_MAX_LAYERS];
-  bool fused_mlp = false;  // FC1 + GELU + FC2 + LayerScale residual in one kernel (mlp.cu)
   // proj / FC2 with the following LayerNorm in their epilogue (gemm_resid_ln_kernel): D = 384 at
   // large M only (the kernel owns whole rows: one CTA per 128-row block)
   GemmPlan proj_rl[VPE_MAX_LAYERS], fc2_rl[VPE_MAX_LAYERS];
@@ -149,18 +146,6 @@ extern "C" int vpe_vit_create(const vpe_vit_config* cfg, const vpe_vit_weights* 
         return fail(rc);
     }
   }
-  {
-    // Opt-in (VPE_FUSED_MLP=1): correct (tests/test_gpu_kernels.py::test_fused_mlp) but measured
-    // slower than the FC1 / FC2 pair at C2 (70.9 vs 52 us per layer): with the 96 KB X block
-    // resident, the W1 ring only holds 8 KB k-blocks of N = 64 MMAs, and per-k-block barrier
-    // overhead dominates (tools/mlp_trace.py: 24 H MMAs take ~2650 clk instead of ~1100).
-    const char* e = getenv("VPE_FUSED_MLP");
-    v->fused_mlp = e && e[0] == '1';
-    for (int l = 0; l < L && v->fused_mlp; ++l)
-      if (plan_mlp(&v->mlp[l], v->xln, M, D, Hd, static_cast<const __nv_bfloat16*>(w->fc1_w[l]), w->fc1_b[l],
-                   static_cast<const __nv_bfloat16*>(w->fc2_w[l]), w->fc2_b[l], w->ls2[l], v->resid) != VPE_OK)
-        v->fused_mlp = false;  // shapes the fused kernel does not cover keep the GEMM pair
-  }
   *out = v;
   return VPE_OK;
 }
@@ -227,14 +212,9 @@ static int vit_blocks_impl(vpe_vit* v, void* const* taps, cudaStream_t s) {
     VPE_TRY(launch_attention(v->attn, s));
     VPE_TRY(launch_gemm(v->proj_g[l], s));
     VPE_TRY(launch_layernorm(v->resid, M, D, w.ln2_w[l], w.ln2_b[l], c.ln_eps, v->xln, nullptr, nullptr, nullptr, s));
-    if (v->fused_mlp) {
-      VPE_TRY(launch_mlp(v->mlp[l], s));
-      count_launches(6);
-    } else {
-      VPE_TRY(launch_gemm(v->fc1_g[l], s));
-      VPE_TRY(launch_gemm(v->fc2_g[l], s));
-      count_launches(7);
-    }
+    VPE_TRY(launch_gemm(v->fc1_g[l], s));
+    VPE_TRY(launch_gemm(v->fc2_g[l], s));
+    count_launches(7);
   }
   VPE_TRY(launch_layernorm(v->resid, M, D, w.norm_w, w.norm_b, c.ln_eps, static_cast<__nv_bfloat16*>(taps[3]),
                            nullptr, nullptr, nullptr, s));

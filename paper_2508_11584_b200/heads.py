@@ -81,11 +81,12 @@ def _p(x):
 class DepthHead:
     """DepthAnything DPT neck + depth head over the 4 tap labels."""
 
-    labels = ("layer{0}", "layer{1}", "layer{2}", "final")
+    kind = "b200_dpt"
 
     def __init__(self, W: dict, cfg: ModelConfig, resolution: int, batch: int, device="cuda"):
         self.device = torch.device(device)
         self.resolution, self.batch = resolution, batch
+        self.tap_labels = cfg.backbone.tap_labels
         dp, D = cfg.dpt, cfg.backbone.dim
         F = dp.fusion
         pk = _Packer(self.device)
@@ -137,6 +138,20 @@ class DepthHead:
         check(lib.vpe_dpt_create(C.byref(cc), C.byref(wc), C.byref(h)), "vpe_dpt_create")
         self._h, self._keep, self._wc = h, pk.keep, wc
 
+    # -- engine-facing backend interface (shared by every head kind) -------------------------
+    def subscriptions(self) -> tuple[str, ...]:
+        return self.tap_labels
+
+    def outputs(self, debug: bool = False) -> dict[str, torch.Tensor]:
+        R, B, dev = self.resolution, self.batch, self.device
+        out = {"depth": torch.zeros(B, R, R, device=dev)}
+        if debug:  # pre-final-ReLU map (parity grading only)
+            out["depth_pre"] = torch.zeros(B, R, R, device=dev)
+        return out
+
+    def run(self, views: dict, outs: dict, stream=None) -> None:
+        self.forward([views[l] for l in self.tap_labels], outs["depth"], outs.get("depth_pre"), stream)
+
     def forward(self, taps, depth, depth_pre=None, stream=None):
         ptrs = (C.c_void_p * 4)(*[_p(t) for t in taps])
         check(lib.vpe_dpt_forward(self._h, ptrs, C.c_void_p(_p(depth)), C.c_void_p(_p(depth_pre)),
@@ -153,8 +168,11 @@ class DepthHead:
 class SegHead:
     """BN + 1x1 linear classifier + bilinear upsample + argmax over the `final` label."""
 
+    kind = "b200_linseg"
+
     def __init__(self, W: dict, cfg: ModelConfig, resolution: int, batch: int, device="cuda"):
         self.device = torch.device(device)
+        self.resolution, self.batch = resolution, batch
         self.classes = cfg.seg_classes
         D = cfg.backbone.dim
         s = W["seg.bn.weight"].double() / torch.sqrt(W["seg.bn.running_var"].double() + cfg.seg_bn_eps)
@@ -172,6 +190,16 @@ class SegHead:
         torch.cuda.synchronize(self.device)
         check(lib.vpe_seg_create(C.byref(cc), C.byref(wc), C.byref(h)), "vpe_seg_create")
         self._h, self._keep, self._wc = h, pk.keep, wc
+
+    def subscriptions(self) -> tuple[str, ...]:
+        return ("final",)
+
+    def outputs(self, debug: bool = False) -> dict[str, torch.Tensor]:
+        R, B = self.resolution, self.batch
+        return {"labels": torch.zeros(B, R, R, dtype=torch.uint8, device=self.device)}
+
+    def run(self, views: dict, outs: dict, stream=None) -> None:
+        self.forward(views["final"], outs["labels"], stream=stream)
 
     def forward(self, final, labels, logits=None, stream=None):
         check(lib.vpe_seg_forward(self._h, C.c_void_p(_p(final)), C.c_void_p(_p(labels)), C.c_void_p(_p(logits)),
@@ -202,6 +230,8 @@ DET_SPLIT = 2  # det 3x3 conv weights as hi+lo bf16 (tensor-core fp32 accumulati
 class DetHead:
     """RPN-style head: 3x3 conv + ReLU, 1x1 cls / bbox, decode, top-k, NMS over `final`."""
 
+    kind = "b200_det"
+
     def __init__(self, W: dict, cfg: ModelConfig, resolution: int, batch: int, device="cuda"):
         self.device = torch.device(device)
         dc = cfg.det
@@ -227,7 +257,13 @@ class DetHead:
         check(lib.vpe_det_create(C.byref(cc), C.byref(wc), C.byref(h)), "vpe_det_create")
         self._h, self._keep, self._wc = h, pk.keep, wc
 
-    def outputs(self):
+    def subscriptions(self) -> tuple[str, ...]:
+        return ("final",)
+
+    def run(self, views: dict, outs: dict, stream=None) -> None:
+        self.forward(views["final"], outs, stream=stream)
+
+    def outputs(self, debug: bool = False):
         post, B, dev = self.dc.post_nms_top_n, self.batch, self.device
         return {"boxes": torch.zeros(B, post, 4, device=dev), "scores": torch.zeros(B, post, device=dev),
                 "index": torch.zeros(B, post, dtype=torch.int64, device=dev),
@@ -246,3 +282,11 @@ class DetHead:
             self._h = None
 
     __del__ = close
+
+
+# backend descriptor kind (registry ModelCard.backend["kind"]) -> head class
+HEAD_BACKENDS = {DepthHead.kind: DepthHead, SegHead.kind: SegHead, DetHead.kind: DetHead}
+# the paper's example deployment by short head name
+BUILTIN_HEADS = {"depth": DepthHead.kind, "seg": SegHead.kind, "det": DetHead.kind}
+# which canonical weight group (weights.make_weights ``heads=``) a backend kind reads
+WEIGHT_GROUP = {DepthHead.kind: "depth", SegHead.kind: "seg", DetHead.kind: "det"}

@@ -22,18 +22,20 @@ def active_backend(force_pure: bool | None = None) -> str:
     return "compiled"
 
 
-def _addr_size(buf):
-    """(address, nbytes) of a writable buffer-protocol object or a tensor."""
+def _export(buf):
+    """(address, nbytes, keepalive) of a writable buffer-protocol object or a host tensor. The
+    keepalive objects pin the buffer export for the AtomicBuffer's lifetime, so the owner cannot
+    be resized or unmapped under the atomics (the reference's typed memoryview does the same)."""
     if hasattr(buf, "data_ptr") and hasattr(buf, "untyped_storage"):
         if buf.is_cuda:
             raise ValueError("AtomicBuffer needs host memory")
-        return buf.data_ptr(), buf.numel() * buf.element_size()
+        return buf.data_ptr(), buf.numel() * buf.element_size(), (buf,)
     mv = memoryview(buf)
     if mv.readonly:
         raise ValueError("buffer must be writable")
     mv = mv.cast("B")
     cbuf = (C.c_char * mv.nbytes).from_buffer(mv)
-    return C.addressof(cbuf), mv.nbytes
+    return C.addressof(cbuf), mv.nbytes, (mv, cbuf)
 
 
 class AtomicBuffer:
@@ -44,7 +46,7 @@ class AtomicBuffer:
 
     def __init__(self, buf):
         self._buf = buf  # keep the owner alive
-        self._addr, self._size = _addr_size(buf)
+        self._addr, self._size, self._pin = _export(buf)
         if lib.vpe_atomic_check_base(C.c_void_p(self._addr), self._size) != 0:
             raise ValueError("buffer base address must be 8-byte aligned")
 
@@ -80,6 +82,7 @@ class AtomicBuffer:
         return out.value
 
     def close(self) -> None:
+        self._pin = ()  # drop the buffer export (the owner may be resized / unmapped again)
         self._buf = None
         self._addr, self._size = 0, 0
 

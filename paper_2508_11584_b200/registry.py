@@ -124,22 +124,26 @@ def validate_deployment(fm: ModelCard, heads: list[ModelCard]) -> list[Mismatch]
     return report
 
 
-def demo_cards(model_cfg, resolution: int, batch: int = 1) -> tuple[ModelCard, list[ModelCard]]:
+def demo_cards(model_cfg, resolution: int, batch: int = 1, rates: dict | None = None) -> tuple[ModelCard, list[ModelCard]]:
     """The paper's example deployment: FM with 4 labelled outputs, depth head on
-    all four, seg and det heads on ``final``."""
+    all four, seg and det heads on ``final``. ``rates`` sets the cards' default_rate per head
+    name ("depth_dpt", "seg_linear", "det_rpn")."""
     from .config import tokens
     bb = model_cfg.backbone
     T = tokens(resolution)
+    rates = rates or {}
     feat = tuple(TensorSpec(l, DType.BF16, (batch, T, bb.dim)) for l in bb.tap_labels)
     img = (TensorSpec("image", DType.U8, (batch, 3, resolution, resolution)),)
-    fm = ModelCard(f"dinov2_{bb.name}", 1, "foundation", img, feat, {"kind": "b200_vit", "dim": bb.dim,
-                                                                      "depth": bb.depth, "resolution": resolution})
+    fm = ModelCard(f"dinov2_{bb.name}", 1, "foundation", img, feat,
+                   {"kind": "b200_vit", "model": bb.name, "dim": bb.dim, "depth": bb.depth, "resolution": resolution})
     R = resolution
+    post = model_cfg.det.post_nms_top_n
     depth = ModelCard("depth_dpt", 1, "head", feat, (TensorSpec("depth", DType.F32, (batch, R, R)),),
-                      {"kind": "b200_dpt"}, None, bb.tap_labels)
+                      {"kind": "b200_dpt"}, rates.get("depth_dpt"), bb.tap_labels)
     seg = ModelCard("seg_linear", 1, "head", feat[-1:], (TensorSpec("labels", DType.U8, (batch, R, R)),),
-                    {"kind": "b200_linseg", "classes": model_cfg.seg_classes}, None, ("final",))
+                    {"kind": "b200_linseg", "classes": model_cfg.seg_classes}, rates.get("seg_linear"), ("final",))
     det = ModelCard("det_rpn", 1, "head", feat[-1:],
-                    (TensorSpec("boxes", DType.F32, (batch, model_cfg.det.post_nms_top_n, 4)),),
-                    {"kind": "b200_det"}, None, ("final",))
+                    (TensorSpec("boxes", DType.F32, (batch, post, 4)), TensorSpec("scores", DType.F32, (batch, post)),
+                     TensorSpec("index", DType.I64, (batch, post)), TensorSpec("count", DType.I32, (batch,))),
+                    {"kind": "b200_det"}, rates.get("det_rpn"), ("final",))
     return fm, [depth, seg, det]

@@ -34,55 +34,6 @@ def test_linear_bf16(ops, device, M, N, K, bn):
     assert rel_l2(out, ref) < 8e-3  # bf16 output rounding
 
 
-@pytest.mark.parametrize("M,N,K,bn", [(16400, 1536, 384, -256), (16400, 384, 1536, -192), (1025, 1152, 384, -192),
-                                        (300, 384, 384, -128), (16400, 384, 384, -256)])
-@pytest.mark.parametrize("act", [0, 1])
-def test_linear_pair(ops, device, M, N, K, bn, act):
-    """CTA-pair (cta_group::2) GEMM: 256-row tiles split over two SMs, M tails, N tails."""
-    g = torch.Generator(device="cpu").manual_seed(M + N + K + act)
-    a = torch.randn(M, K, generator=g).to(device, torch.bfloat16)
-    w = (torch.randn(N, K, generator=g) * 0.05).to(device, torch.bfloat16)
-    bias = torch.randn(N, generator=g).to(device)
-    out = ops.linear(a, w, bias=bias, act=act, bn=bn)
-    torch.cuda.synchronize()
-    ref = a.float() @ w.float().t() + bias
-    if act:
-        ref = F.gelu(ref)
-    assert rel_l2(out, ref) < 8e-3
-
-
-def test_linear_pair_resid(ops, device):
-    g = torch.Generator().manual_seed(7)
-    M, N, K = 16400, 384, 1536
-    a = torch.randn(M, K, generator=g).to(device, torch.bfloat16)
-    w = (torch.randn(N, K, generator=g) * 0.02).to(device, torch.bfloat16)
-    bias = torch.randn(N, generator=g).to(device)
-    ls = torch.rand(N, generator=g).to(device) + 0.5
-    h = torch.randn(M, N, generator=g).to(device)
-    ref = h + ls * (a.float() @ w.float().t() + bias)
-    ops.linear(a, w, bias=bias, scale=ls, out=h, kind=ops.EPI_RESID, bn=-192)
-    torch.cuda.synchronize()
-    assert rel_l2(h, ref) < 1e-4
-
-
-@pytest.mark.parametrize("M", [16400, 1025, 300, 128])
-def test_fused_mlp(ops, device, M):
-    """resid += ls2 * (GELU(x W1^T + b1) W2^T + b2) with the hidden activation kept on-chip."""
-    g = torch.Generator().manual_seed(M)
-    D, Hd = 384, 1536
-    x = torch.randn(M, D, generator=g).to(device, torch.bfloat16)
-    w1 = (torch.randn(Hd, D, generator=g) * 0.05).to(device, torch.bfloat16)
-    w2 = (torch.randn(D, Hd, generator=g) * 0.03).to(device, torch.bfloat16)
-    b1, b2 = torch.randn(Hd, generator=g).to(device), torch.randn(D, generator=g).to(device)
-    ls2 = (torch.rand(D, generator=g) + 0.5).to(device)
-    resid = torch.randn(M, D, generator=g).to(device)
-    inc = ls2 * (F.gelu(x.float() @ w1.float().t() + b1) @ w2.float().t() + b2)
-    ref = resid + inc
-    ops.mlp(x, w1, b1, w2, b2, ls2, resid)
-    torch.cuda.synchronize()
-    assert rel_l2(resid - (ref - inc), inc) < 8e-3  # hidden rounded to bf16 like the unfused path
-
-
 def test_linear_gelu_and_resid(ops, device):
     g = torch.Generator().manual_seed(1)
     M, N, K = 1025, 1536, 384
@@ -118,7 +69,8 @@ def test_linear_split_precision(ops, device):
     assert rel_l2(out.cpu().double(), ref) < 1e-5
 
 
-@pytest.mark.parametrize("B,T,heads", [(1, 257, 6), (1, 1025, 6), (2, 1370, 12), (1, 128, 2), (3, 200, 4)])
+@pytest.mark.parametrize("B,T,heads", [(1, 257, 6), (1, 1025, 6), (2, 1370, 12), (1, 128, 2), (3, 200, 4),
+                                       (16, 1025, 6), (16, 1370, 12), (8, 1370, 16)])
 def test_attention(ops, device, B, T, heads):
     D = heads * 64
     g = torch.Generator().manual_seed(T)
@@ -128,7 +80,10 @@ def test_attention(ops, device, B, T, heads):
     ref = torch.softmax(q @ k.transpose(-1, -2) / 8.0, -1) @ v
     ref = ref.transpose(1, 2).reshape(B * T, D)
     torch.cuda.synchronize()
-    assert rel_l2(out, ref) < 1.5e-2
+    e = rel_l2(out, ref)
+    print(f"attention B={B} T={T} H={heads}: rel-L2 {e:.3e}")
+    # measured ~3e-3 (bf16 output rounding + bf16 P); 6e-3 catches a 2x regression
+    assert e < 6e-3
 
 
 @pytest.mark.parametrize("B,T,heads", [(2, 1025, 6), (1, 1370, 12)])
@@ -147,7 +102,9 @@ def test_attention_rising_scores(ops, device, B, T, heads):
     ref = torch.softmax(q @ k.transpose(-1, -2) / 8.0, -1) @ v
     ref = ref.transpose(1, 2).reshape(B * T, D)
     torch.cuda.synchronize()
-    assert rel_l2(out, ref) < 1.5e-2
+    e = rel_l2(out, ref)
+    print(f"attention rising scores B={B} T={T}: rel-L2 {e:.3e}")
+    assert e < 6e-3
 
 
 def test_layernorm(ops, device):
@@ -199,25 +156,6 @@ def test_bilinear_align_corners(ops, device, Hi, Ho, C):
     torch.cuda.synchronize()
     err = (out.float() - ref).abs()
     assert (err <= ref.abs() * 2 ** -7 + 1e-6).all(), err.max().item()
-
-
-@pytest.mark.parametrize("M,N,act", [(16400, 1152, 0), (16400, 1536, 1), (1025, 1152, 0), (300, 1536, 1)])
-def test_linear_ln_fused_matches_unfused(ops, device, M, N, act):
-    """GEMM with LayerNorm(x) built in its prologue == LayerNorm kernel + GEMM, bit for bit (same
-    LN rounding in ln.cuh, same bf16 A, same MMA order); the tap LN output likewise."""
-    g = torch.Generator().manual_seed(M + N)
-    D = 384
-    x = (torch.randn(M, D, generator=g) * 3 + 0.5).to(device)
-    lw, lb = (torch.randn(D, generator=g) * 0.5 + 1).to(device), torch.randn(D, generator=g).to(device)
-    tw, tb = torch.randn(D, generator=g).to(device), torch.randn(D, generator=g).to(device)
-    w = (torch.randn(N, D, generator=g) * 0.05).to(device, torch.bfloat16)
-    bias = torch.randn(N, generator=g).to(device)
-    out, tap = ops.linear_ln(x, lw, lb, 1e-6, w, bias=bias, act=act, tap_w=tw, tap_b=tb)
-    xln, tap_ref = ops.layernorm(x, lw, lb, 1e-6, tw, tb)
-    ref = ops.linear(xln, w, bias=bias, act=act, bn=256)
-    torch.cuda.synchronize()
-    assert torch.equal(tap, tap_ref)
-    assert torch.equal(out, ref), (out.float() - ref.float()).abs().max().item()
 
 
 @pytest.mark.parametrize("M,K,tap", [(16400, 384, False), (16400, 1536, True), (1025, 384, True), (300, 1536, False)])

@@ -292,4 +292,8 @@ class VpeAdapter:
     def close(self):
         self.ch.close()
         from paper_2508_11584_b200 import arena as ar
+        self.dst.arena.close()
+        if hasattr(self.dst.arena, "unlink"):
+            self.dst.arena.unlink()
         ar.forget_allocation(f"{self.ns}.dst")
+        assert not ar.shm_census(self.ns), ar.shm_census(self.ns)

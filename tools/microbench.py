@@ -66,20 +66,6 @@ def main():
             t_f = timeit_graph(lambda: _ops.linear_resid_ln(a, w, bias, ls, resid, lw, lb, 1e-6))
             print(json.dumps(dict(K=K, gemm_resid_us=t_g, layernorm_us=t_ln, fused_us=t_f)), flush=True)
         return
-    if args.only == "ln":  # LayerNorm + GEMM vs the GEMM with LayerNorm in its prologue
-        M, D = 16400, 384
-        x = torch.randn(M, D, device=dev)
-        lw, lb = torch.ones(D, device=dev), torch.zeros(D, device=dev)
-        for N, act in ((1152, 0), (1536, 1)):
-            w = (torch.randn(N, D, device=dev) * 0.05).to(torch.bfloat16)
-            bias = torch.zeros(N, device=dev)
-            xln = torch.empty(M, D, device=dev, dtype=torch.bfloat16)
-            out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
-            t_ln = timeit_graph(lambda: _ops.layernorm(x, lw, lb))
-            t_g = timeit_graph(lambda: _ops.linear(xln, w, bias=bias, out=out, act=act, bn=256))
-            t_f = timeit_graph(lambda: _ops.linear_ln(x, lw, lb, 1e-6, w, bias=bias, act=act))
-            print(json.dumps(dict(N=N, act=act, layernorm_us=t_ln, gemm_us=t_g, fused_us=t_f)), flush=True)
-        return
     if args.only == "seg":
         for (B, h, C, cp) in [(16, 32, 150, 160), (1, 32, 150, 160)]:
             lg = torch.randn(B, h * h, cp, device=dev)

@@ -11,7 +11,7 @@ from paper_2508_11584_b200 import _ops
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("what", choices=["attention", "gemm", "mlp"])
+    p.add_argument("what", choices=["attention", "gemm"])
     p.add_argument("--B", type=int, default=16)
     p.add_argument("--T", type=int, default=1025)
     p.add_argument("--H", type=int, default=6)
@@ -28,14 +28,6 @@ def main():
         D = a.H * 64
         qkv = torch.randn(a.B * a.T, 3 * D, device=dev).to(torch.bfloat16)
         fn = lambda: _ops.attention(qkv, a.B, a.T, D, a.H)
-    elif a.what == "mlp":
-        D, Hd = 384, 1536
-        x = torch.randn(a.M, D, device=dev).to(torch.bfloat16)
-        w1 = (torch.randn(Hd, D, device=dev) * 0.05).to(torch.bfloat16)
-        w2 = (torch.randn(D, Hd, device=dev) * 0.03).to(torch.bfloat16)
-        b1, b2, ls2 = torch.zeros(Hd, device=dev), torch.zeros(D, device=dev), torch.ones(D, device=dev)
-        resid = torch.zeros(a.M, D, device=dev)
-        fn = lambda: _ops.mlp(x, w1, b1, w2, b2, ls2, resid)
     else:
         x = torch.randn(a.M, a.K, device=dev).to(torch.bfloat16)
         w = (torch.randn(a.N, a.K, device=dev) * 0.02).to(torch.bfloat16)
