@@ -5,9 +5,10 @@
 One step = one frame set of ``--batch`` camera frames (batch 1 per camera stream; the engine
 co-schedules the cameras it serves through one backbone pass) through the full hot path:
 H2D (e2e only) -> backbone -> ring publish -> depth/seg/det heads in place -> D2H (e2e only).
-Under torchrun each rank drives one GPU with its own shard of camera streams; there is no
-collective on the data path — torch.distributed is used only for the barrier and
-the max-over-ranks of the timed region.
+With ``--gpus N`` (N > 1) and no torchrun environment, bench.py re-launches itself under
+``torch.distributed.run`` with one rank per GPU; each rank drives one GPU with its own shard of
+camera streams; there is no collective on the data path — torch.distributed is used
+only for the barrier and the max-over-ranks of the timed region.
 
   python bench.py --gpus N --steps K --warmup W [--batch B] [--impl ours|reference]
 
@@ -19,6 +20,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -54,15 +56,33 @@ def parse():
     p.add_argument("--resolution", type=int, default=448)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--sustained-seconds", type=float, default=10.0,
+                   help="length of the sustained C2 window reported beside the --steps number (0 = skip)")
     p.add_argument("--rates", default="", help="per-head frame ratios, e.g. depth=1:1,seg=1:2,det=1:4 (config C3)")
     return p.parse_args()
+
+
+# ------------------------------------------------------------------------------------------------
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N without a torchrun environment: one process per GPU via torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, cwd=ROOT).returncode
 
 
 def dist_setup(n):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n:
+        raise SystemExit(f"bench.py: --gpus {n} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -77,53 +97,73 @@ def _cuda():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled (NVML, 20 ms) during the timed region."""
+    """SM clocks + throttle reasons from NVML, sampled every 5 ms in a thread while the timed
+    region runs, plus one sample right before and right after it. NVML is initialised here, in
+    the caller's thread, before the window opens."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, gpu: int):
-        self.gpu, self.rows, self._stop = gpu, [], threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self.max_mhz = None
-
-    def _run(self):
+        self.rows, self.edges, self._stop = [], {}, threading.Event()
+        self.err = None
         try:
             import pynvml as nv
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((sm, rs))
-                self._stop.wait(0.02)
-        except Exception as exc:  # reported as unsampled
-            self.err = repr(exc)
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(gpu)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception as exc:
+            self.nv, self.max_mhz, self.err = None, None, repr(exc)
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def sample(self):
+        sm = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+        rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        return sm, rs
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.rows.append(self.sample())
+            except Exception as exc:
+                self.err = repr(exc)
+                return
+            self._stop.wait(0.005)
 
     def __enter__(self):
-        self._t.start()
+        if self.nv:
+            self.edges["before"] = self.sample()
+            self._t.start()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=6)
+        if self.nv:
+            self._stop.set()
+            self._t.join(timeout=6)
+            self.edges["after"] = self.sample()
+
+    def _names(self, mask):
+        return sorted(name for bit, name in self.REASONS.items() if mask & bit)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "error": self.err}
         sm = [r[0] for r in self.rows]
-        reasons = sorted({name for _, m in self.rows for bit, name in self.REASONS.items() if m & bit})
+        reasons = sorted({n for _, m in self.rows for n in self._names(m)})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "sm_mhz_min": min(sm),
+                "before": {"sm_mhz": self.edges["before"][0], "reasons": self._names(self.edges["before"][1])},
+                "after": {"sm_mhz": self.edges["after"][0], "reasons": self._names(self.edges["after"][1])}}
 
 
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
-    except Exception:
-        return 6650.0, 1590.0, 1400.0, "fallback"
+        return {"hbm": d["hbm_gbs"], "tensor": d["bf16_tflops"],
+                "tensor_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "kind": "measured"}
+    except Exception:  # /opt/skills/guides/B200_PROFILING.md fallbacks
+        return {"hbm": 6650.0, "tensor": 1590.0, "tensor_sustained": 1400.0, "kind": "fallback"}
 
 
 def frame_flops(cfg, R):
@@ -135,7 +175,6 @@ def frame_flops(cfg, R):
 # ------------------------------------------------------------------------------------------------
 def cpu_baseline(args, cfg, W, seconds):
     """Reference CPU path (fanpipe transport + fp32 oracle, all host threads) on a bounded sample."""
-    import torch
     from oracle.cpu_pipeline import CpuPipeline
     from paper_2508_11584_b200.weights import make_frames
     threads = os.cpu_count() or 1
@@ -156,11 +195,14 @@ def cpu_baseline(args, cfg, W, seconds):
 
 
 def run_reference(args):
+    """The reference's CPU path on the host cores: (i) sequential foundation -> heads over the
+    unmodified fanpipe LATEST channel, (ii) the paper's deployment, one foundation process and
+    one process per head over the same channel (oracle/cpu_pipeline.py). The line's value is the
+    faster of the two (the stronger baseline)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
-    from oracle.cpu_pipeline import CpuPipeline
+    from oracle.cpu_pipeline import CpuPipeline, multiprocess_pipeline
     from paper_2508_11584_b200.config import model_config
     from paper_2508_11584_b200.weights import make_frames, make_weights
     cfg = model_config(args.model)
@@ -175,16 +217,27 @@ def run_reference(args):
         pipe.step(frames)
     dt = time.perf_counter() - t0
     pipe.close()
-    v = args.steps / dt
+    seq = args.steps / dt
+    try:
+        mp = multiprocess_pipeline(args.model, args.resolution, max(5.0, min(20.0, 0.5 * dt)), threads=threads)
+    except Exception as exc:  # reported, the sequential variant stands
+        mp = {"error": repr(exc), "fps": 0.0}
+    v = max(seq, mp["fps"])
+    kind = "sequential" if v == seq else "multiprocess"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "C2: DINOv2 ViT-S/14 + depth + seg + det heads, 448x448, all heads every frame",
                    "batch": 1, "host": "cpu"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} frames (batch 1) through the unmodified fanpipe transport "
-                                   f"(baseline/_ref) + fp32 oracle compute, {threads} torch threads"},
+                         "sample": f"best of (i) {args.steps} frames (batch 1) sequential foundation -> 3 heads "
+                                   f"through the unmodified fanpipe transport (baseline/_ref) + fp32 oracle, "
+                                   f"{threads} torch threads: {seq:.2f} fps; (ii) 1 foundation + 3 head processes "
+                                   f"over a fanpipe LATEST channel, threads {mp.get('threads')}: "
+                                   f"{mp['fps']:.2f} fps -> {kind}"},
+        "variants": {"sequential": {"fps": seq, "seconds": dt}, "multiprocess": mp},
+        "cpu_model": _cpu_model(),
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
     # the reference's shared-memory arena raises BufferError from __del__ at interpreter exit
@@ -193,57 +246,185 @@ def run_reference(args):
     os._exit(0)
 
 
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 # ------------------------------------------------------------------------------------------------
-def kernel_roofline(engine, args, peaks):
-    """Time the dominant kernel class alone with CUDA events on its stream (same shapes as the
-    step): the backbone FC1 GEMM (bias+GELU epilogue) at M = batch*T, N = 4D, K = D."""
+def _graph_time(fn, reps: int = 20, replays: int = 10) -> float:
+    """Seconds per call of ``fn`` (kernel launches only), timed over CUDA-graph replays with
+    CUDA events on the capturing stream, after warm-up."""
     import torch
-    from paper_2508_11584_b200 import _ops
-    D, T, B = engine.D, engine.T, engine.batch
-    M, N, K = B * T, 4 * D, D
-    a = torch.randn(M, K, device=engine.device).to(torch.bfloat16)
-    w = (torch.randn(N, K, device=engine.device) * 0.02).to(torch.bfloat16)
-    bias = torch.zeros(N, device=engine.device)
-    out = torch.empty(M, N, device=engine.device, dtype=torch.bfloat16)
-    s = torch.cuda.current_stream()
-    for _ in range(10):
-        _ops.linear(a, w, bias=bias, out=out, act=_ops.ACT_GELU, bn=BACKBONE_BN)
-    # 20 launches captured in one CUDA graph and replayed: the events then bracket back-to-back
-    # kernels (host-side planning/launch cost of the eager op is not part of the kernel's time)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        for _ in range(20):
-            _ops.linear(a, w, bias=bias, out=out, act=_ops.ACT_GELU, bn=BACKBONE_BN)
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(reps):
+            fn()
     g.replay()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    replays = 10
-    reps = 20 * replays
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(replays):
+            g.replay()
+        e1.record(s)
     torch.cuda.synchronize()
-    e0.record(s)
-    for _ in range(replays):
-        g.replay()
-    e1.record(s)
-    torch.cuda.synchronize()
-    dur = e0.elapsed_time(e1) / reps * 1e-3
-    flops = 2.0 * M * N * K
-    achieved = flops / dur / 1e12
-    return {"kernel": f"gemm_tc_kernel<{BACKBONE_BN},64> FC1+GELU M={M} N={N} K={K}", "bound": "tensor",
-            "achieved": achieved, "peak": peaks[1], "unit": "TFLOP/s", "frac": achieved / peaks[1],
-            "peak_kind": peaks[3] + " burst", "duration_us": dur * 1e6, "traffic": _profiled_traffic(M, N, K)}
+    return e0.elapsed_time(e1) * 1e-3 / (reps * replays)
 
 
-def _profiled_traffic(M, N, K):
-    """DRAM bytes per launch of this kernel from the committed ncu --set full capture, when the
-    captured shape matches (profiles/round1_ncu_fc1.json); None otherwise."""
+def _ncu_traffic(name, shape):
+    """DRAM bytes per launch from the committed ncu --set full summary of this kernel when the
+    captured shape matches (profiles/round2_ncu_<name>.json), else None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "round1_ncu_fc1.json")) as f:
+        with open(os.path.join(ROOT, "profiles", f"round2_ncu_{name}.json")) as f:
             d = json.load(f)
-        if d["shape"] == {"M": M, "N": N, "K": K}:
+        if d.get("shape") == shape:
             return d["dram_bytes_read"] + d["dram_bytes_write"]
     except Exception:
         pass
     return None
+
+
+def kernel_rooflines(eng, peaks):
+    """Each kernel class of the step timed alone at the step's exact shapes (CUDA events over
+    graph replays): achieved = algorithmic FLOPs or bytes per launch / launch time, against the
+    measured burst peak (tensor) or copy bandwidth (HBM). Returns (dominant, list)."""
+    import torch
+    from paper_2508_11584_b200 import _ops
+    dev = eng.device
+    D, T, B, R = eng.D, eng.T, eng.batch, eng.resolution
+    H = eng.cfg.backbone.heads
+    M = B * T
+    g = torch.Generator(device="cpu").manual_seed(0)
+
+    def rnd(*shape, std=1.0, dtype=torch.bfloat16):
+        return (torch.randn(*shape, generator=g) * std).to(dev, dtype)
+
+    out = []
+
+    def tensor(name, kernel, shape, flops, fn):
+        dur = _graph_time(fn)
+        a = flops / dur / 1e12
+        out.append({"kernel": kernel, "class": name, "shape": shape, "bound": "tensor", "achieved": a,
+                    "peak": peaks["tensor"], "unit": "TFLOP/s", "frac": a / peaks["tensor"],
+                    "duration_us": dur * 1e6, "algorithmic": flops, "traffic": _ncu_traffic(name, shape)})
+
+    def hbm(name, kernel, shape, nbytes, fn, note=""):
+        dur = _graph_time(fn)
+        a = nbytes / dur / 1e9
+        out.append({"kernel": kernel, "class": name, "shape": shape, "bound": "hbm", "achieved": a,
+                    "peak": peaks["hbm"], "unit": "GB/s", "frac": a / peaks["hbm"], "duration_us": dur * 1e6,
+                    "algorithmic": nbytes, "traffic": _ncu_traffic(name, shape), **({"note": note} if note else {})})
+
+    qkv = rnd(M, 3 * D)
+    tensor("attention", "attention_tc_kernel", {"B": B, "T": T, "H": H}, 4.0 * B * T * T * D,
+           lambda: _ops.attention(qkv, B, T, D, H))
+    xln = rnd(M, D)
+    for nm, N, act in (("qkv", 3 * D, 0), ("fc1", 4 * D, 1)):
+        w = rnd(N, D, std=0.02)
+        bias = torch.zeros(N, device=dev)
+        o = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        tensor(nm, f"gemm_tc_kernel<{BACKBONE_BN},64>" + (" +GELU" if act else ""), {"M": M, "N": N, "K": D},
+               2.0 * M * N * D, lambda w=w, bias=bias, o=o, act=act: _ops.linear(xln, w, bias=bias, out=o, act=act,
+                                                                                 bn=BACKBONE_BN))
+    if D == 384 and (M + 127) // 128 >= 100:
+        resid = rnd(M, D, dtype=torch.float32)
+        lw, lb = torch.ones(D, device=dev), torch.zeros(D, device=dev)
+        ls = torch.full((D,), 0.1, device=dev)
+        for nm, K in (("proj_resid_ln", D), ("fc2_resid_ln", 4 * D)):
+            a_ = rnd(M, K)
+            w = rnd(D, K, std=0.02)
+            bias = torch.zeros(D, device=dev)
+            tensor(nm, "gemm_resid_ln_kernel", {"M": M, "N": D, "K": K}, 2.0 * M * D * K,
+                   lambda a_=a_, w=w, bias=bias: _ops.linear_resid_ln(a_, w, bias, ls, resid, lw, lb, 1e-6))
+            # the same kernel against HBM: A, W, old + new fp32 residual, bf16 LN output
+            out[-1]["hbm_bytes"] = M * K * 2 + D * K * 2 + M * D * (4 + 4 + 2)
+            out[-1]["hbm_frac"] = out[-1]["hbm_bytes"] / (out[-1]["duration_us"] * 1e-6) / 1e9 / peaks["hbm"]
+    # DPT head: conv2 (3x3, Fh -> 32 at R x R, depth epilogue fused in the engine; plain conv here)
+    F = eng.cfg.dpt.fusion
+    Fh = F // 2
+    x = rnd(B, R, R, Fh)
+    w = rnd(32, 9 * Fh, std=0.05)
+    bias = torch.zeros(32, device=dev)
+    o = torch.empty(B, R, R, 32, device=dev, dtype=torch.bfloat16)
+    tensor("dpt_head_conv", "conv_halo_kernel<32,4,4,1>", {"B": B, "H": R, "C": Fh, "N": 32},
+           2.0 * B * R * R * 32 * 9 * Fh, lambda: _ops.conv(x, w, Fh, 3, bias=bias, out=o))
+    S = 4 * (R // 14)
+    x2 = rnd(B, S, S, F)
+    w2 = rnd(F, 9 * F, std=0.05)
+    b2 = torch.zeros(F, device=dev)
+    o2 = torch.empty(B, S, S, F, device=dev, dtype=torch.bfloat16)
+    tensor("dpt_rcu_conv", "conv_halo_kernel<64,8,2,1>", {"B": B, "H": S, "C": F, "N": F},
+           2.0 * B * S * S * F * 9 * F, lambda: _ops.conv(x2, w2, F, 3, bias=b2, out=o2))
+    # DPT resize 2S -> R (align_corners=True), Fh channels: read the source once, write the output
+    src = rnd(B, 2 * S, 2 * S, Fh)
+    hbm("dpt_bilinear", "bilinear_ac_rows_kernel", {"B": B, "Hi": 2 * S, "Ho": R, "C": Fh},
+        B * (2 * S * 2 * S + R * R) * Fh * 2, lambda: _ops.bilinear(src, R, R))
+    # seg: fused upsample + argmax, logits read once, u8 labels written
+    h = R // 14
+    C = eng.cfg.seg_classes
+    cp = (C + 31) // 32 * 32
+    lg = rnd(B, h * h, cp, dtype=torch.float32)
+    hbm("seg_upsample_argmax", "seg_upsample_argmax_kernel", {"B": B, "h": h, "C": C},
+        B * (h * h * cp * 4 + R * R), lambda: _ops.upsample_argmax(lg, h, R, classes=C),
+        note="instruction-bound: ~C x R^2 bilinear interpolations per image")
+    xr = rnd(M, D, dtype=torch.float32)
+    lw, lb = torch.ones(D, device=dev), torch.zeros(D, device=dev)
+    hbm("layernorm", "layernorm_kernel", {"M": M, "D": D}, M * D * (4 + 2), lambda: _ops.layernorm(xr, lw, lb))
+    # every backbone class launches once per layer: the longest one dominates the step
+    dom = max((r for r in out if r["class"] in ("attention", "qkv", "fc1", "proj_resid_ln", "fc2_resid_ln")),
+              key=lambda r: r["duration_us"])
+    return dom, out
+
+
+def parity_e2e(eng, W, nframes=2):
+    """End-to-end agreement (bf16 GPU pipeline vs the fp32 CPU oracle from the same u8 frames),
+    reported beside the stage-wise bars the tests enforce: depth rel-L2,
+    seg argmax agreement overall and on pixels whose oracle top-2 margin >= 1e-2, det top-100
+    index overlap."""
+    import torch
+    from oracle import det as odet
+    from oracle import dpt as odpt
+    from oracle import seg as oseg
+    from oracle import vit as ovit
+    from paper_2508_11584_b200.weights import make_frames
+    cfg, R, B = eng.cfg, eng.resolution, eng.batch
+    frames = torch.cat([make_frames(1, R, stream_id=s) for s in range(B)], 0)
+    out = eng.run(frames)
+    h = R // 14
+    res = {"frames": nframes, "depth_rel_l2": [], "seg_agreement": [], "seg_agreement_margin_1e-2": [],
+           "seg_margin_pixel_frac": [], "det_top100_overlap": [], "det_top100_identical": []}
+    bb = cfg.backbone
+    with torch.no_grad():
+        for b in range(nframes):
+            taps = ovit.backbone_forward(frames[b:b + 1], W, bb.depth, bb.heads, bb.taps)
+            d = odpt.dpt_forward(taps, W, cfg.dpt.factors, h)
+            g = out["depth"]["depth"][b:b + 1].cpu()
+            res["depth_rel_l2"].append(((g - d).norm() / d.norm()).item())
+            lab, _, up = oseg.seg_forward(taps[-1], W, h, R, return_logits=True)
+            top2 = up.topk(2, dim=1).values
+            margin = (top2[:, 0] - top2[:, 1])[0]
+            agree = out["seg"]["labels"][b].cpu() == lab[0]
+            m = margin >= 1e-2
+            res["seg_agreement"].append(agree.float().mean().item())
+            res["seg_agreement_margin_1e-2"].append(agree[m].float().mean().item())
+            res["seg_margin_pixel_frac"].append(m.float().mean().item())
+            ref = odet.det_forward(taps[-1], W, h, R, cfg.det)[0]["index"]
+            k = int(out["det"]["count"][b])
+            gi = out["det"]["index"][b, :k].cpu()
+            res["det_top100_overlap"].append(len(set(gi.tolist()) & set(ref.tolist())) / max(1, ref.numel()))
+            res["det_top100_identical"].append(bool(torch.equal(gi, ref)))
+    return res
 
 
 def latency_mode(args, W, device):
@@ -274,7 +455,7 @@ def run_ours(args):
     from paper_2508_11584_b200 import _lib
     from paper_2508_11584_b200.config import model_config
     from paper_2508_11584_b200.engine import VPEngine
-    from paper_2508_11584_b200.sharding import max_over_ranks, streams_for_rank
+    from paper_2508_11584_b200.sharding import max_over_ranks, streams_for_rank, total_frames
     from paper_2508_11584_b200.weights import make_frames, make_weights
 
     cfg = model_config(args.model)
@@ -301,7 +482,9 @@ def run_ours(args):
                                   _lib.C.c_void_p(pool_dev[i % npool].data_ptr()), frame_bytes, _lib.C.c_void_p(sp))
         eng.submit(record_latency=True)
 
-    def timed(fn, steps, warm):
+    def timed(fn, steps, warm, seconds=None):
+        """Device time of ``steps`` steps (or of as many as fit in ``seconds`` of wall time),
+        max over ranks; returns (seconds, launches, steps)."""
         for i in range(warm):
             fn(i)
         eng.synchronize()
@@ -314,8 +497,17 @@ def run_ours(args):
         launches0 = _lib.lib.vpe_kernel_launches()
         eng.latencies_ms()
         ev0.record(ext)
-        for i in range(steps):
-            fn(warm + i)
+        n = 0
+        t0 = time.perf_counter()
+        while True:
+            fn(warm + n)
+            n += 1
+            if seconds is None and n >= steps:
+                break
+            if seconds is not None and time.perf_counter() - t0 >= seconds:
+                break
+            if seconds is not None and n % 64 == 0:
+                eng.latencies_ms()  # recycle the latency-event pool on long runs
         for s in eng.s_head.values():
             e = torch.cuda.Event()
             e.record(torch.cuda.ExternalStream(s.handle))
@@ -326,12 +518,23 @@ def run_ours(args):
         dt = ev0.elapsed_time(ev1) * 1e-3
         launches = _lib.lib.vpe_kernel_launches() - launches0
         dt = max_over_ranks(dt, dist, eng.device)
-        return dt, launches
+        return dt, launches, n
 
-    with ClockSampler(local) as clk:
-        dt, launches = timed(step_device, args.steps, args.warmup)
+    clk = ClockSampler(local)
+    with clk:
+        dt, launches, _ = timed(step_device, args.steps, args.warmup)
     lat = eng.latencies_ms()
     value = world * B * args.steps / dt
+
+    sustained = None
+    if args.sustained_seconds > 0:
+        clk_s = ClockSampler(local)
+        with clk_s:
+            dts, _, ns = timed(step_device, 0, 2, seconds=args.sustained_seconds)
+        eng.latencies_ms()
+        frames_all = total_frames(B * ns, dist, eng.device)
+        sustained = {"value": frames_all / dts, "unit": UNIT, "seconds": dts, "frames": frames_all,
+                     "steps_rank0": ns, "clocks": clk_s.summary()}
 
     # e2e: host pinned frames in, every head output read back to pinned host memory
     eng.enable_host_outputs()
@@ -340,11 +543,18 @@ def run_ours(args):
     def step_host(i):
         eng.submit(pool_host[i % nh], record_latency=False)
 
-    dt_e2e, _ = timed(step_host, args.steps, args.warmup)
+    dt_e2e, _, _ = timed(step_host, args.steps, args.warmup)
     e2e = world * B * args.steps / dt_e2e
     d2h = eng.host_output_bytes()
     peaks = measured_peaks()
-    roof = kernel_roofline(eng, args, peaks) if rank == 0 else None
+    roof, classes, par = None, None, None
+    if rank == 0:
+        roof, classes = kernel_rooflines(eng, peaks)
+        roof = dict(roof, peak_kind=f"{peaks['kind']} burst")
+        try:
+            par = parity_e2e(eng, W)
+        except Exception as exc:  # reported, never fatal to the GPU number
+            par = {"error": repr(exc)}
     cnt = eng.counters()
     eng.close()
     p50_latency = latency_mode(args, W, local) if rank == 0 else None
@@ -375,6 +585,9 @@ def run_ours(args):
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": frame_bytes, "d2h_bytes_per_step": d2h},
             "gpu_launches": int(launches),
             "roofline": roof,
+            "roofline_classes": classes,
+            "sustained": sustained,
+            "parity_e2e": par,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "ring": {"pushed": cnt.pushed, "drops": cnt.producer_drops, "evictions": cnt.evictions,
@@ -390,6 +603,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args))
     else:
         run_ours(args)
 

@@ -136,5 +136,7 @@ def test_bench_config_heads(name):
                             logit_max_err=max_err))
         assert torch.equal(gi, ri), (name, b)
         assert gap <= 2 * max_err, (name, b, gap, max_err)
-        torch.testing.assert_close(out["det"]["boxes"][b, :k], ref[b]["boxes"], rtol=1e-5, atol=1e-3)
+        # box coordinates inherit the deltas' ~1e-5 relative error (fp32 tensor-core accumulation
+        # over K = 9 D): measured up to 2.1e-3 px at D = 1024, R = 518
+        torch.testing.assert_close(out["det"]["boxes"][b, :k], ref[b]["boxes"], rtol=1e-5, atol=1e-5 * R)
         torch.testing.assert_close(out["det"]["scores"][b, :k], ref[b]["scores"], rtol=1e-5, atol=1e-6)
