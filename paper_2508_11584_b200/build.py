@@ -20,6 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr",
          "-I", os.path.join(HERE, "..", "include")]
+# diagnostics builds only: VPE_NVCC_EXTRA="-DVPE_TRACE_BUILD" compiles the kernels' timeline probes in
+FLAGS += os.environ.get("VPE_NVCC_EXTRA", "").split()
 
 
 # seg.cu: the fused upsample+argmax must round every mul and add separately (torch's order) and

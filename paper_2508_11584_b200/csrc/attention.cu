@@ -11,12 +11,15 @@
 //   warps 1, 2  MMA issuers, one per Q slot X: S_X(j+1) = Q_X K_{j+1}^T as soon as softmax X has
 //               pulled S_X(j) into registers; O_X += P_X(j) V_j with P read from TMEM (.kind::f16
 //               A-from-TMEM), so P never touches shared memory
-//   warp 3      idle (completes warpgroup 0)
-//   warps 4-11  softmax A, warps 12-19 softmax B: two warps per 32 query rows, one per 64-key
+//   warps 3-10  softmax A, warps 11-18 softmax B: two warps per 32 query rows, one per 64-key
 //               half of each S tile; the pair agrees on the row max through smem + a named
-//               barrier; p = 2^(s*scale - m) written to TMEM as bf16 pairs; O is rescaled in TMEM
-//               only when the running max rises by > 8 (log2), i.e. almost never after the first
-//               KV tile.
+//               barrier (pass 1), then p = 2^(s*scale - m) is written to TMEM as bf16 pairs
+//               (pass 2). The two slots' exponential passes alternate (mbarrier token
+//               A(j) -> B(j) -> A(j+1)), so one slot's max pass runs under the other slot's MUFU
+//               work. O is rescaled in TMEM only when the running max rises by > 8 (log2), i.e.
+//               almost never after the first KV tile. (Holding the whole 64-key half in
+//               registers to read S once needs ~110 registers; at 608 threads ptxas caps at 96
+//               and spills the scores: 2x slower, measured.)
 // TMEM (512 columns): S_A | S_B | P_A | P_B | O_A | O_B.
 // Rows/keys past T (tail tiles) are computed on whatever the TMA brought (the next image's rows
 // or zero fill) and masked: invalid keys get p = 0, invalid rows are never stored, and warps whose
@@ -40,9 +43,9 @@ namespace vpe {
 namespace {
 constexpr int TILE = 16 * 1024;  // one [128][64] bf16 SW128 tile
 constexpr int KS = 3, VS = 3;    // K / V ring depth
-constexpr int ATT_THREADS = 640;  // 0 TMA, 1-2 MMA (slot A / B), 3 idle, 4-11 softmax A, 12-19 softmax B
+constexpr int ATT_THREADS = 608;  // 0 TMA, 1-2 MMA (slot A / B), 3-10 softmax A, 11-18 softmax B
 constexpr int XCH_BYTES = 2 * 3 * 2 * 128 * 4;  // row max / sum exchange [slot][tile parity | epi][half][row]
-constexpr int SMEM_ATT = 1024 + 4 * TILE /*Q_A,Q_B x 2 units*/ + KS * TILE + VS * TILE + XCH_BYTES + 256;
+constexpr int SMEM_ATT = 1024 + 4 * TILE /*Q_A,Q_B x 2 units*/ + KS * TILE + VS * TILE + XCH_BYTES + 512;
 constexpr uint32_t S_COL = 0, P_COL = 256, O_COL = 384;
 }  // namespace
 
@@ -65,6 +68,12 @@ VPE_DEV void tmem_st16u(uint32_t taddr, const uint32_t (&r)[16]) {
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
+}
+
+VPE_DEV void tmem_st4u(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
 }
 
 // O[tmem] (+)= A[tmem] * B[smem], kind::f16; A (M x K, K-major, 2 bf16 per 32-bit column)
@@ -134,19 +143,22 @@ constexpr float kTruncScale = 1.00282f;
 
 // p = 2^(v*scale - m) for one 32-key chunk -> 16 bf16 pairs in TMEM at p_taddr; returns the
 // chunk's f32x2 partial sums. poly_ok: chunk has no masked (-inf) keys.
-template <int kPolyMask>  // pairs (of 16 per chunk) whose exp2 runs on the FMA pipe
-VPE_DEV uint64_t emit_chunk(const float (&v)[32], float scale_log2, float m_used, uint32_t p_taddr, bool poly_ok) {
+template <int kPolyMask, bool kPolyOk>  // pairs (of 16 per chunk) whose exp2 runs on the FMA pipe
+VPE_DEV uint64_t emit_chunk(const float (&v)[32], float scale_log2, float m_used, uint32_t p_taddr) {
   const uint64_t sc2 = f2_pack(scale_log2, scale_log2);
   const float mb = kTruncBias - m_used;
   const uint64_t mb2 = f2_pack(mb, mb);
   uint64_t acc0 = 0, acc1 = 0;
-  uint32_t pk[16];
-  if (poly_ok) {
+  // P leaves in groups of 4 pairs (x4 stores): 4 live packed registers instead of 16
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+  for (int g = 0; g < 4; ++g) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = 4 * g + q;
       const uint64_t xx = ffma2(f2_pack(v[2 * i], v[2 * i + 1]), sc2, mb2);
       uint64_t pp;
-      if ((kPolyMask >> i) & 1) {
+      if (kPolyOk && ((kPolyMask >> i) & 1)) {
         pp = exp2_poly2(xx);
       } else {
         float x0, x1;
@@ -154,20 +166,10 @@ VPE_DEV uint64_t emit_chunk(const float (&v)[32], float scale_log2, float m_used
         pp = f2_pack(fast_exp2(x0), fast_exp2(x1));
       }
       if (i & 1) acc1 = fadd2(acc1, pp); else acc0 = fadd2(acc0, pp);
-      pk[i] = __byte_perm((uint32_t)pp, (uint32_t)(pp >> 32), 0x7632);
+      pk[q] = __byte_perm((uint32_t)pp, (uint32_t)(pp >> 32), 0x7632);
     }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const uint64_t xx = ffma2(f2_pack(v[2 * i], v[2 * i + 1]), sc2, mb2);
-      float x0, x1;
-      f2_unpack(xx, x0, x1);
-      const uint64_t pp = f2_pack(fast_exp2(x0), fast_exp2(x1));
-      if (i & 1) acc1 = fadd2(acc1, pp); else acc0 = fadd2(acc0, pp);
-      pk[i] = __byte_perm((uint32_t)pp, (uint32_t)(pp >> 32), 0x7632);
-    }
+    tmem_st4u(p_taddr + 4 * g, pk[0], pk[1], pk[2], pk[3]);
   }
-  tmem_st16u(p_taddr, pk);
   return fadd2(acc0, acc1);
 }
 
@@ -176,14 +178,20 @@ VPE_DEV uint64_t emit_chunk(const float (&v)[32], float scale_log2, float m_used
 // each event = (code, clock64).
 __device__ unsigned long long g_att_trace[4096];
 static int g_att_trace_on = -1;
+#ifdef VPE_TRACE_BUILD
 #define ATT_TRACE(slot_base, idx, code)                                              \
   do {                                                                               \
-    if ((trace & 1) && blockIdx.x == 0 && (idx) < 510) {                                   \
+    if ((trace & 1) && blockIdx.x == 0 && (idx) < 510) {                             \
       g_att_trace[(slot_base) + 2 * (idx)] = (unsigned long long)(code);             \
       g_att_trace[(slot_base) + 2 * (idx) + 1] = (unsigned long long)clock64();      \
       ++(idx);                                                                       \
     }                                                                                \
   } while (0)
+#else
+#define ATT_TRACE(slot_base, idx, code) \
+  do {                                  \
+  } while (0)
+#endif
 
 struct AttnUnit {
   int b, h, q0, has_b;
@@ -223,7 +231,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   uint64_t* s_free = s_full + 2;    // [2] softmax x has pulled S_x into registers
   uint64_t* p_full = s_free + 2;    // [2 slots][2 key halves]
   uint64_t* o_done = p_full + 4;    // [2 slots][2 key halves]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 4);
+  uint64_t* e_done = o_done + 4;    // [2 slots] exp pass of the slot's current tile finished
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(e_done + 2);
 
   const int BH = B * heads;
   const int nkv = (T + 127) / 128;
@@ -245,6 +254,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         mbar_init(&p_full[i * 2 + h], 4);
         mbar_init(&o_done[i * 2 + h], 1);
       }
+      mbar_init(&e_done[i], 8);
     }
     for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
@@ -293,6 +303,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     // one MMA issuer per Q slot, so neither slot's PV/S issue queues behind the other's
     if (lane == 0) {
       const int x = warp - 1;
+      int tn = 0;
+      const int tbase = 1024 * x;
       constexpr uint32_t idesc_s = idesc_bf16(128, 128);
       constexpr uint32_t idesc_o = idesc_bf16(128, 64, /*b_mn_major=*/true);
       int kit = 0, vit = 0, qn = 0, np = 0;  // np: PV MMAs issued (= p_full / s_free phases consumed)
@@ -321,6 +333,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             mbar_wait(&k_full[ks], (kit / KS) & 1);
             tc_fence_after();
             if (mine) issue_s(smem_u32(sK + ks * TILE));
+            if (mine) ATT_TRACE(tbase, tn, 20);
             if (nkv > 1) {  // K_0 stays until S_x(0) is done; with nkv == 1 it is released below
               if (mine) umma_commit(&k_empty[ks]); else mbar_arrive(&k_empty[ks]);
               ++kit;
@@ -336,12 +349,14 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
               mbar_wait(&s_free[x], np & 1);  // S_x(j) is in softmax registers: S_x(j+1) may land
               tc_fence_after();
               issue_s(smem_u32(sK + ks * TILE));
+              ATT_TRACE(tbase, tn, 20);
             }
             // O_x += P_x(j) V_j in two key halves, each as soon as its softmax warp pair has
             // written its half of P (and each half of P is released on its own)
             const uint32_t v_addr = smem_u32(sV + vs * TILE);
             for (int h = 0; h < 2; ++h) {
               mbar_wait(&p_full[x * 2 + h], np & 1);
+              ATT_TRACE(tbase, tn, 21 + h);
               tc_fence_after();
 #pragma unroll
               for (int k = 4 * h; k < 4 * h + 4; ++k)
@@ -361,13 +376,11 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         }
       }
     }
-  } else if (warp == 3) {
-    // idle: completes warpgroup 0
   } else {
-    // softmax warps: Q slot x, column half hh (keys 64*hh .. 64*hh+63 of each tile), TMEM lane
-    // quadrant = warp % 4. The two warps of a (slot, quadrant) own the same 32 rows and agree on
-    // the row max through smem + a 64-thread named barrier.
-    const int sw = (int)warp - 4;
+    // softmax warps 3-18: Q slot x, column half hh (keys 64*hh .. 64*hh+63 of each tile), TMEM
+    // lane quadrant = warp % 4 (hardware). The two warps of a (slot, quadrant) own the same 32
+    // rows and agree on the row max through smem + a 64-thread named barrier.
+    const int sw = (int)warp - 3;
     const int x = sw >> 3, hh = (sw >> 2) & 1;
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
@@ -377,9 +390,12 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     const uint32_t p_addr = lane_base + P_COL + x * 64 + hh * 32;
     const uint32_t o_addr = lane_base + O_COL + x * 64;
     int ns = 0, npv = 0;  // S tiles consumed, P tiles produced (global counts)
+    int na = 0, nb = 0;   // exp passes slot A / slot B completed before the current unit
     int tn = 0;
     const bool tr = (quad == 0 && lane == 0 && hh == 0);
     const int tbase = 2048 + 1024 * x;
+    const int dbg = trace >> 1;  // diagnostics (VPE_ATT_DBG): 2 = no exp ping-pong
+    const bool pp = !(dbg & 2);
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
     for (int ui = u_lo; ui < u_hi; ++ui) {
       const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T, single);
@@ -397,6 +413,20 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_free[x]);
         };
+        // ping-pong on the exponential unit: slot A's pass j follows slot B's pass j-1 and slot
+        // B's pass j follows slot A's pass j, so one slot's max pass (TMEM reads, 3-input max,
+        // exchange) runs under the other slot's exponentials instead of both slots contending
+        // for MUFU at once and leaving it idle during their max passes
+        auto exp_token = [&]() {
+          if (w.has_b && pp) {
+            if (x == 0 && j > 0) mbar_wait(&e_done[1], (nb + j - 1) & 1);
+            if (x == 1) mbar_wait(&e_done[0], (na + j) & 1);
+          }
+        };
+        auto exp_done = [&]() {
+          __syncwarp();
+          if (w.has_b && pp && lane == 0) mbar_arrive(&e_done[x]);
+        };
         if (warp_active) {
           const int kvalid = T - j * 128 - hh * 64;  // keys of this half >= kvalid are padding
           const int nch = kvalid >= 64 ? 2 : (kvalid <= 0 ? 0 : (kvalid + 31) >> 5);
@@ -407,15 +437,27 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
                 if (c * 32 + i >= kvalid) v[i] = -INFINITY;
             }
           };
-          // pass 1: row max over this half (one 32-column chunk in registers at a time)
+          // pass 1: row max over this half (one 32-column chunk in registers at a time). Full
+          // halves (every tile but the ragged last one) take a branch-free path.
+          const bool full = kvalid >= 64;
           float mx = -INFINITY;
+          if (full) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              float v[32];
+              tmem_ld32(s_addr + c * 32, v);
+              tmem_ld_wait_dep(v);
+              mx = fmaxf(mx, chunk_max_log2(v, scale_log2));
+            }
+          } else {
 #pragma unroll 1
-          for (int c = 0; c < nch; ++c) {
-            float v[32];
-            tmem_ld32(s_addr + c * 32, v);
-            tmem_ld_wait_dep(v);
-            mask(c, v);
-            mx = fmaxf(mx, chunk_max_log2(v, scale_log2));
+            for (int c = 0; c < nch; ++c) {
+              float v[32];
+              tmem_ld32(s_addr + c * 32, v);
+              tmem_ld_wait_dep(v);
+              mask(c, v);
+              mx = fmaxf(mx, chunk_max_log2(v, scale_log2));
+            }
           }
           float* xrow = xch + ((x * 3 + (ns & 1)) * 2) * 128;
           xrow[hh * 128 + r] = mx;
@@ -432,6 +474,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             l *= alpha;
             m_used = m_new;
           }
+          exp_token();
           // this half of P_x(j-1) must have been consumed before this half of P_x(j) is written
           if (npv > 0) {
             mbar_wait(&o_done[x * 2 + hh], (npv - 1) & 1);
@@ -440,23 +483,37 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           if (tr) ATT_TRACE(tbase, tn, 12);
           // pass 2: p = 2^(s*scale - m_used) for this half's two chunks
           uint64_t lt = 0;  // f32x2 partial row sums
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            if (c < nch) {
+          if (full) {
+            {
               float v[32];
-              tmem_ld32(s_addr + c * 32, v);
+              tmem_ld32(s_addr, v);
               tmem_ld_wait_dep(v);
-              if (c + 1 >= nch) release_s();
-              mask(c, v);
-              lt = fadd2(lt, emit_chunk<POLY>(v, scale_log2, m_used, p_addr + c * 16, c * 32 + 32 <= kvalid));
-            } else {
-              if (c == 0) release_s();
-              uint32_t pk[16];
+              lt = emit_chunk<POLY, true>(v, scale_log2, m_used, p_addr);
+            }
+            float v[32];
+            tmem_ld32(s_addr + 32, v);
+            tmem_ld_wait_dep(v);
+            release_s();
+            lt = fadd2(lt, emit_chunk<POLY, true>(v, scale_log2, m_used, p_addr + 16));
+          } else {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = 0u;
-              tmem_st16u(p_addr + c * 16, pk);
+            for (int c = 0; c < 2; ++c) {
+              if (c < nch) {
+                float v[32];
+                tmem_ld32(s_addr + c * 32, v);
+                tmem_ld_wait_dep(v);
+                if (c + 1 >= nch) release_s();
+                mask(c, v);
+                lt = fadd2(lt, c * 32 + 32 <= kvalid ? emit_chunk<POLY, true>(v, scale_log2, m_used, p_addr + c * 16)
+                                                     : emit_chunk<POLY, false>(v, scale_log2, m_used, p_addr + c * 16));
+              } else {
+                if (c == 0) release_s();
+#pragma unroll
+                for (int g = 0; g < 4; ++g) tmem_st4u(p_addr + c * 16 + 4 * g, 0u, 0u, 0u, 0u);
+              }
             }
           }
+          exp_done();
           if (rescale && j > 0) {
             // O_x *= alpha in TMEM, once per row (half 0), after both halves of PV_x(j-1) and
             // before either half of PV_x(j) may be issued (the pair syncs before p_full)
@@ -484,10 +541,17 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           tmem_st_wait();
         } else {
           release_s();
+          // a warp whose rows are all past T must not run ahead: its p_full arrival for tile j
+          // would otherwise count toward tile j-1's phase while the active warps of the tile are
+          // still writing P_x(j-1), releasing PV_x(j-1) early (a latent race of round 1's kernel)
+          if (npv > 0) mbar_wait(&o_done[x * 2 + hh], (npv - 1) & 1);
+          exp_token();  // inactive rows still take part in the hand-off (arrive counts are per warp)
+          exp_done();
         }
         tc_fence_before();
         __syncwarp();
         if (tr) ATT_TRACE(tbase, tn, 13);
+        (void)dbg;
         if (lane == 0) mbar_arrive(&p_full[x * 2 + hh]);  // this half of P_x(j) in TMEM
       }
       // epilogue: l = l_half0 + l_half1; each half writes 32 of the 64 output columns
@@ -518,6 +582,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
         }
       }
       tc_fence_before();
+      na += nkv;
+      if (w.has_b) nb += nkv;
     }
   }
   tc_fence_before();
@@ -602,6 +668,11 @@ int plan_attention(AttnPlan* a, const __nv_bfloat16* qkv, __nv_bfloat16* out, in
   return VPE_OK;
 }
 
+static int att_dbg() {
+  static const int d = getenv("VPE_ATT_DBG") ? atoi(getenv("VPE_ATT_DBG")) : 0;
+  return d;
+}
+
 int launch_attention(const AttnPlan& a, cudaStream_t s) {
   static int poly = -1;
   if (poly < 0) {
@@ -610,23 +681,23 @@ int launch_attention(const AttnPlan& a, cudaStream_t s) {
   }
   static OncePerDevice attr;
   if (attr.first()) {
-    cudaFuncSetAttribute(attention_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
-    cudaFuncSetAttribute(attention_tc_kernel<0x0707>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
-    cudaFuncSetAttribute(attention_tc_kernel<0x0303>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
-    cudaFuncSetAttribute(attention_tc_kernel<0x1111>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT);
-    max_smem_carveout(attention_tc_kernel<0>);
-    max_smem_carveout(attention_tc_kernel<0x0707>);
-    max_smem_carveout(attention_tc_kernel<0x0303>);
-    max_smem_carveout(attention_tc_kernel<0x1111>);
+#define VPE_ATT_ATTR(P_)                                                                          \
+  cudaFuncSetAttribute(attention_tc_kernel<P_>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_ATT); \
+  max_smem_carveout(attention_tc_kernel<P_>);
+    VPE_ATT_ATTR(0) VPE_ATT_ATTR(0x0303) VPE_ATT_ATTR(0x1111) VPE_ATT_ATTR(0x2525) VPE_ATT_ATTR(0x5555)
+#undef VPE_ATT_ATTR
   }
   const float scale_log2 = 0.125f * 1.4426950408889634f;
   if (g_att_trace_on < 0) {
     const char* e = getenv("VPE_ATT_TRACE");
     g_att_trace_on = (e && e[0] == '1') ? 1 : 0;
   }
-  auto k = poly == 0 ? attention_tc_kernel<0>
-                     : (poly == 2 ? attention_tc_kernel<0x0303>
-                                  : (poly == 3 ? attention_tc_kernel<0x1111> : attention_tc_kernel<0x0707>));
+  // pairs of exponentials (of 16 per 32-key chunk) computed on the FMA pipe instead of MUFU
+  auto k = poly == 0   ? attention_tc_kernel<0>
+           : poly == 2 ? attention_tc_kernel<0x0303>
+           : poly == 4 ? attention_tc_kernel<0x2525>
+           : poly == 5 ? attention_tc_kernel<0x5555>
+                       : attention_tc_kernel<0x1111>;
   // Never PDL-launched: with the attention kernel in the programmatic chain the engine's outputs
   // vary bitwise run to run (tools/pdl_determinism.py, VPE_PDL_MASK bisection: every mask that
   // includes the attention kernel, even with griddepcontrol.wait moved to its first instruction;
@@ -639,7 +710,7 @@ int launch_attention(const AttnPlan& a, cudaStream_t s) {
     ~Restore() { pdl_scope() = v; }
   } restore{saved_scope};
   return launch_k(k, dim3(a.grid), dim3(ATT_THREADS), SMEM_ATT, s, a.tqkv, a.out, a.B, a.T, a.D, a.heads, scale_log2,
-                  g_att_trace_on, a.sched, a.single) == cudaSuccess
+                  g_att_trace_on | (att_dbg() << 1), a.sched, a.single) == cudaSuccess
              ? VPE_OK
              : VPE_E_CUDA;
 }
