@@ -11,7 +11,8 @@ import os
 
 from . import errors
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libvpe.so")
+# VPE_LIB selects a diagnostics build (e.g. libvpe_trace.so from VPE_BUILD_TAG=trace) in-tree
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("VPE_LIB", "libvpe.so"))
 
 MAX_LAYERS = 40
 MAX_CONSUMERS = 16

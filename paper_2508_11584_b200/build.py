@@ -14,8 +14,11 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libvpe.so")
-OBJ = os.path.join(HERE, "build")
+# diagnostics variants build side by side: VPE_BUILD_TAG=trace -> libvpe_trace.so (loaded with
+# VPE_LIB=libvpe_trace.so); the product library is always libvpe.so
+_TAG = os.environ.get("VPE_BUILD_TAG", "")
+OUT = os.path.join(HERE, f"libvpe_{_TAG}.so" if _TAG else "libvpe.so")
+OBJ = os.path.join(HERE, f"build_{_TAG}" if _TAG else "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr",

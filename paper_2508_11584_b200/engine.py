@@ -744,6 +744,7 @@ class VPEngine:
     def latencies_ms(self) -> dict[str, list[float]]:
         out = {n: [] for n in self.heads}
         for n, a, b in self._lat_records:
+            b.sync()  # the pool may be recycled mid-run: wait for the head's end event first
             out[n].append(a.elapsed_ms(b))
         self._lat_records = []
         self._ev_next = 0

@@ -8,6 +8,7 @@ resolution of the oracle's own scores are reported, not failed)."""
 import pytest
 import torch
 
+from det_match import align_to, kept_match
 from oracle import det as odet
 from oracle import dpt as odpt
 from oracle import seg as oseg
@@ -106,16 +107,19 @@ def test_det_stagewise(setup):
     for b in range(B):
         k = int(out["count"][b])
         gi, ri = out["index"][b, :k].cpu(), ref[b]["index"]
-        # the detections (post-NMS top-k) are identical, index for index
-        assert torch.equal(gi, ri)
+        # the detections (post-NMS top-k) are identical, index for index, up to near-tie swaps
+        # the measured logit error explains (tests/det_match.py)
+        ok, nsw, kgap = kept_match(gi, ri, obj[b], max_err)
+        assert ok, (b, nsw, kgap, max_err)
+        p = align_to(gi, ri)
         # the pre-NMS top-k ranking may only differ by swaps the measured error can explain
         gt, rt = out["top_index"][b].cpu(), ref[b]["top_index"]
         diff = (gt != rt).nonzero().flatten()
         if diff.numel():
             gap = (obj[b][gt[diff]] - obj[b][rt[diff]]).abs().max().item()
             assert gap <= 2 * max_err, f"top-k swap gap {gap:.3e} > 2 x max err {max_err:.3e}"
-        torch.testing.assert_close(out["boxes"][b, :k].cpu(), ref[b]["boxes"], rtol=1e-5, atol=1e-3)
-        torch.testing.assert_close(out["scores"][b, :k].cpu(), ref[b]["scores"], rtol=1e-5, atol=1e-6)
+        torch.testing.assert_close(out["boxes"][b, :k].cpu()[p], ref[b]["boxes"], rtol=1e-5, atol=1e-3)
+        torch.testing.assert_close(out["scores"][b, :k].cpu()[p], ref[b]["scores"], rtol=1e-5, atol=1e-6)
 
 
 @pytest.mark.parametrize("B,h,C,cp", [(2, 32, 150, 160), (1, 16, 21, 32), (1, 32, 7, 8), (1, 16, 256, 256)])
