@@ -117,12 +117,14 @@ VPE_DEV float chunk_max_log2(const float (&v)[32], float scale_log2) {
   return fmax3(m0, m1, fmaxf(v[30], v[31])) * scale_log2;
 }
 
-// 2^x for a pair, x <= 8, on the FMA pipe: x = n + f (n = rint(x), |f| <= 1/2), 2^f by a cubic
-// (max rel. error 1.4e-4, far below the bf16 rounding of P), 2^n by adding n to the exponent.
+// 2^x for a pair on the FMA pipe: x = n + f (n = rint(x), |f| <= 1/2), 2^f by a cubic (max rel.
+// error 1.4e-4, far below the bf16 rounding of P), 2^n by adding n to the exponent field of each
+// 32-bit half (two IMADs; a 64-bit shift/or cost six instructions). Valid for x < 128; x is
+// clamped at -126 (p(f) may be just below 1, so n = -127 would borrow into the sign bit: NaN).
 VPE_DEV uint64_t exp2_poly2(uint64_t x) {
   float x0, x1;
   f2_unpack(x, x0, x1);
-  x = f2_pack(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+  x = f2_pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
   const float kMagic = 12582912.f;  // 1.5 * 2^23: x + kMagic holds rint(x) in its low mantissa bits
   const uint64_t j = fadd2(x, f2_pack(kMagic, kMagic));
   const uint64_t nf = fadd2(j, f2_pack(-kMagic, -kMagic));
@@ -130,9 +132,12 @@ VPE_DEV uint64_t exp2_poly2(uint64_t x) {
   uint64_t p = ffma2(f, f2_pack(0.05502927f, 0.05502927f), f2_pack(0.24225698f, 0.24225698f));
   p = ffma2(p, f, f2_pack(0.69325305f, 0.69325305f));
   p = ffma2(p, f, f2_pack(0.99995134f, 0.99995134f));
-  const uint32_t jl = (uint32_t)j, jh = (uint32_t)(j >> 32);
-  const uint32_t pl = (uint32_t)p, ph = (uint32_t)(p >> 32);
-  return ((uint64_t)(ph + (jh << 23)) << 32) | (uint64_t)(pl + (jl << 23));
+  uint32_t jl, jh, pl, ph;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(jl), "=r"(jh) : "l"(j));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(pl), "=r"(ph) : "l"(p));
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(pl + (jl << 23)), "r"(ph + (jh << 23)));
+  return r;
 }
 
 // P in bf16 by truncation (one PRMT per pair). The exponent offset carries +log2(1 + 0.00282),
@@ -300,15 +305,29 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
       }
     }
   } else if (warp == 1 || warp == 2) {
-    // one MMA issuer per Q slot, so neither slot's PV/S issue queues behind the other's
-    if (lane == 0) {
-      const int x = warp - 1;
+    // One MMA issuer warp per Q slot, so neither slot's PV/S issue queues behind the other's.
+    // The whole warp runs the loop and one elected lane issues, with every operand computed by
+    // all lanes before the election, so the descriptors stay in uniform registers (a lone lane-0
+    // thread needed a ~16-instruction R2UR.BROADCAST waterfall per UTCHMMA).
+    {
+      const int x = __shfl_sync(0xffffffffu, (int)warp - 1, 0);
       int tn = 0;
       const int tbase = 1024 * x;
       constexpr uint32_t idesc_s = idesc_bf16(128, 128);
       constexpr uint32_t idesc_o = idesc_bf16(128, 64, /*b_mn_major=*/true);
       int kit = 0, vit = 0, qn = 0, np = 0;  // np: PV MMAs issued (= p_full / s_free phases consumed)
-      const uint32_t s_t = tmem + S_COL + x * 128, p_t = tmem + P_COL + x * 64, o_t = tmem + O_COL + x * 64;
+      const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t s_t = tmem_u + S_COL + x * 128, p_t = tmem_u + P_COL + x * 64, o_t = tmem_u + O_COL + x * 64;
+      const uint32_t sQ_u = __shfl_sync(0xffffffffu, smem_u32(sQ), 0), sK_u = sQ_u + 4 * TILE, sV_u = sK_u + KS * TILE;
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) umma_commit(bar);
+        __syncwarp();
+      };
+      auto arrive = [&](uint64_t* bar) {
+        if (elect_one()) mbar_arrive(bar);
+        __syncwarp();
+      };
+      if (lane != 0) tn = 1 << 20;  // (trace build) lane 0 records
       for (int ui = u_lo; ui < u_hi; ++ui, ++qn) {
         const AttnUnit w = unit_of(__ldg(ulist + ui), BH, heads, T, single);
         const bool mine = (x == 0) || w.has_b;
@@ -317,25 +336,27 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           mbar_wait(&q_full[qi], (qn >> 1) & 1);
           tc_fence_after();
         }
-        const uint32_t q_addr = smem_u32(sQ + qi * TILE);
+        const uint32_t q_addr = sQ_u + qi * TILE;
         // S_x = Q_x K^T. The previous S_x was released (s_free / p_full waited) before the
         // previous PV, so the S_x columns are free here.
         auto issue_s = [&](uint32_t k_addr) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_f16(s_t, smem_desc(q_addr + k * 32, 16, 1024, 2), smem_desc(k_addr + k * 32, 16, 1024, 2), idesc_s,
-                     k > 0);
-          umma_commit(&s_full[x]);
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = smem_desc(q_addr + k * 32, 16, 1024, 2), bd = smem_desc(k_addr + k * 32, 16, 1024, 2);
+            if (elect_one()) umma_f16(s_t, ad, bd, idesc_s, k > 0);
+            __syncwarp();
+          }
+          commit(&s_full[x]);
         };
         for (int j = 0; j < nkv; ++j, ++vit) {
           if (j == 0) {  // S_x(0)
             const int ks = kit % KS;
             mbar_wait(&k_full[ks], (kit / KS) & 1);
             tc_fence_after();
-            if (mine) issue_s(smem_u32(sK + ks * TILE));
+            if (mine) issue_s(sK_u + ks * TILE);
             if (mine) ATT_TRACE(tbase, tn, 20);
             if (nkv > 1) {  // K_0 stays until S_x(0) is done; with nkv == 1 it is released below
-              if (mine) umma_commit(&k_empty[ks]); else mbar_arrive(&k_empty[ks]);
+              if (mine) commit(&k_empty[ks]); else arrive(&k_empty[ks]);
               ++kit;
             }
           }
@@ -348,29 +369,32 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
             if (next) {
               mbar_wait(&s_free[x], np & 1);  // S_x(j) is in softmax registers: S_x(j+1) may land
               tc_fence_after();
-              issue_s(smem_u32(sK + ks * TILE));
+              issue_s(sK_u + ks * TILE);
               ATT_TRACE(tbase, tn, 20);
             }
             // O_x += P_x(j) V_j in two key halves, each as soon as its softmax warp pair has
             // written its half of P (and each half of P is released on its own)
-            const uint32_t v_addr = smem_u32(sV + vs * TILE);
+            const uint64_t vd0 = smem_desc(sV_u + vs * TILE, 1024, 1024, 2);
+            const uint32_t vlo = __shfl_sync(0xffffffffu, (uint32_t)vd0, 0), vhi = (uint32_t)(vd0 >> 32);
             for (int h = 0; h < 2; ++h) {
               mbar_wait(&p_full[x * 2 + h], np & 1);
               ATT_TRACE(tbase, tn, 21 + h);
               tc_fence_after();
 #pragma unroll
-              for (int k = 4 * h; k < 4 * h + 4; ++k)
-                umma_f16_ts(o_t, p_t + k * 8, smem_desc(v_addr + k * 2048, 1024, 1024, 2), idesc_o,
-                            (j > 0 || k > 0) ? 1u : 0u);
-              umma_commit(&o_done[x * 2 + h]);
+              for (int k = 4 * h; k < 4 * h + 4; ++k) {
+                const uint64_t bd = ((uint64_t)vhi << 32) | (vlo + (uint32_t)(k * (2048 >> 4)));
+                if (elect_one()) umma_f16_ts(o_t, p_t + k * 8, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+                __syncwarp();
+              }
+              commit(&o_done[x * 2 + h]);
             }
             ++np;
-            if (next || nkv == 1) umma_commit(&k_empty[ks]);
-            umma_commit(&v_empty[vs]);
-            if (!next) umma_commit(&q_empty[qi]);  // every S_x of the unit issued
+            if (next || nkv == 1) commit(&k_empty[ks]);
+            commit(&v_empty[vs]);
+            if (!next) commit(&q_empty[qi]);  // every S_x of the unit issued
           } else {
-            if (next || nkv == 1) mbar_arrive(&k_empty[ks]);
-            mbar_arrive(&v_empty[vs]);
+            if (next || nkv == 1) arrive(&k_empty[ks]);
+            arrive(&v_empty[vs]);
           }
           if (next || nkv == 1) ++kit;
         }

@@ -58,6 +58,26 @@ VPE_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Warp-converged wait for a whole issuer warp: the loop condition is a warp vote, so ptxas knows
+// every lane leaves together and keeps the warp's uniform values (descriptors, TMEM addresses) in
+// uniform registers afterwards. (The asm-internal branch of mbar_wait looks divergent to ptxas,
+// which then moves every later MMA operand through R2UR.BROADCAST.)
+VPE_DEV bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+VPE_DEV void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  while (!__all_sync(0xffffffffu, mbar_try(bar, parity))) {
+  }
+}
+
 // Same, but the thread may stay suspended in the barrier for up to `ns` (it still resumes as soon
 // as the phase completes): for warps that wait long (epilogue on the accumulator, producer on a
 // free slot). With the default short limit they re-issue try_wait/bra ~100x per wait and steal

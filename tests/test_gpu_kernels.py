@@ -86,14 +86,17 @@ def test_attention(ops, device, B, T, heads):
     assert e < 4e-3
 
 
-@pytest.mark.parametrize("B,T,heads", [(2, 1025, 6), (1, 1370, 12)])
-def test_attention_rising_scores(ops, device, B, T, heads):
+@pytest.mark.parametrize("B,T,heads,top", [(2, 1025, 6, 10.0), (1, 1370, 12, 10.0), (2, 1025, 6, 40.0),
+                                           (1, 300, 2, 400.0)])
+def test_attention_rising_scores(ops, device, B, T, heads, top):
     """Scores that rise along the key axis by more than the kernel's rescale threshold per KV tile,
-    so the running offset moves and O is rescaled in TMEM on every tile (the rare path)."""
+    so the running offset moves and O is rescaled in TMEM (the rare path). top = 10: ~14 (log2)
+    per KV tile, one-pass tiles and redone tiles alternate; top = 40: every one-pass tile is
+    redone; top = 400: single tiles whose exponentials would overflow fp32 before the redo."""
     D = heads * 64
     g = torch.Generator().manual_seed(T + 1)
     qkv = torch.randn(B * T, 3 * D, generator=g) * 0.3
-    ramp = torch.linspace(0, 10, T).repeat(B)                   # key t gets + ramp[t] per dim
+    ramp = torch.linspace(0, top, T).repeat(B)                  # key t gets + ramp[t] per dim
     qkv[:, :D] += 1.0                                           # q . k ~ 64 * ramp -> s/8 ~ 8 * ramp
     qkv[:, D:2 * D] += ramp[:, None]
     qkv = qkv.to(device, torch.bfloat16)

@@ -26,4 +26,13 @@ t0 = min(t for c, t in ev if c)
 for name, lo, hi in (("mmaA", 0, 512), ("mmaB", 512, 1024), ("softA", 1024, 1536), ("softB", 1536, 2048)):
     rows = [(c, t - t0) for c, t in ev[lo:hi] if c]
     print(name, len(rows))
-    print(" ".join(f"{c}@{t}" for c, t in rows[:200]))
+    print(" ".join(f"{c}@{t}" for c, t in rows[:400]))
+
+if os.environ.get("VPE_ATT_DBG", "0") == "32":
+    # per-warp pass start/end (codes 12/17) of softmax warps 3..18
+    for sw in range(16):
+        rows = [(c, t - t0) for c, t in ev[1024 + 64 * sw: 1024 + 64 * (sw + 1)] if c]
+        print(f"warp{sw + 1}", " ".join(f"{c}@{t}" for c, t in rows[:40]))
+    for x in range(2):
+        rows = [(c, t - t0) for c, t in ev[512 * x: 512 * (x + 1)] if c]
+        print(f"mmadone{'AB'[x]}", " ".join(f"{c}@{t}" for c, t in rows[:60]))
