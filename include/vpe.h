@@ -290,6 +290,16 @@ int vpe_op_camera_im2col(const void* frames_hwc_u8, int32_t B, int32_t height, i
 int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32_t Cp, int32_t ks, const void* w,
                 int32_t N, const float* bias, const void* add1, const void* add2, void* out, void* out_relu,
                 int32_t ldo, int32_t act, void* stream);
+/* conv of the resize: 3x3 same-padding conv applied to the bilinear align_corners=True resize of
+ * x [B,Hs,Ws,Cp] (Cp = 32 or 64) to Ho x Wo, the resized map never materialised; out bf16 NHWC
+ * [B,Ho,Wo,ldo] = act(conv + bias). Bit-identical to vpe_op_bilinear followed by vpe_op_conv (DPT
+ * head: modeling_depth_anything.py:288-308). Weights [N = 32, 9*Cp] tap-major, first packed by
+ * vpe_op_conv_up_pack into wpack (3*96*Cp bf16). With w3: the DPT depth epilogue instead,
+ * depth[B,Ho,Wo] f32 = relu(b3 + sum_c relu(conv_c + bias_c) w3_c) */
+int vpe_op_conv_up_pack(const void* w, int32_t Cp, void* wpack, void* stream);
+int vpe_op_conv_up(const void* x, int32_t B, int32_t Hs, int32_t Ws, int32_t Cp, int32_t Ho, int32_t Wo,
+                   const void* wpack, int32_t N, const float* bias, void* out, int32_t ldo, int32_t act,
+                   const float* w3, float b3, float* depth, void* stream);
 int vpe_op_attention(const void* qkv, void* out, int32_t B, int32_t T, int32_t D, int32_t heads, void* stream);
 /* bilinear (align_corners=False) upsample of fp32 logits [B, h*h, cp] (C real classes) to
  * [B, R, R] + argmax over classes -> u8 labels; R = 14 h; torch's rounding and first-index ties

@@ -152,6 +152,8 @@ _SIGS = {
     "vpe_debug_gemm_trace": (i32, [vp, i32]),
     "vpe_op_attention": (i32, [vp, vp, i32, i32, i32, i32, vp]),
     "vpe_op_linear_resid_ln": (i32, [vp, i32, i32, vp, vp, vp, vp, vp, vp, f32, vp, vp, vp, vp, vp]),
+    "vpe_op_conv_up_pack": (i32, [vp, i32, vp, vp]),
+    "vpe_op_conv_up": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, i32, vp, vp, i32, i32, vp, f32, vp, vp]),
     "vpe_op_bilinear": (i32, [vp, i32, i32, i32, i32, i32, vp, i32, i32, vp]),
     "vpe_op_upsample_argmax": (i32, [vp, i32, i32, i32, i32, i32, vp, vp]),
     "vpe_op_layernorm": (i32, [vp, i32, i32, vp, vp, f32, vp, vp, vp, vp, vp]),

@@ -45,6 +45,34 @@ def conv(x: torch.Tensor, w: torch.Tensor, C_real: int, ks: int, bias=None, add1
     return out
 
 
+def conv_up_pack(w: torch.Tensor, stream=None) -> torch.Tensor:
+    """[32, 9*Cp] tap-major bf16 conv weights -> the fused kernel's dy-stacked [3, 96, Cp] layout."""
+    Cp = w.shape[1] // 9
+    wp = torch.empty(3, 96, Cp, device=w.device, dtype=torch.bfloat16)
+    check(lib.vpe_op_conv_up_pack(_p(w), Cp, _p(wp), _s(stream)), "vpe_op_conv_up_pack")
+    return wp
+
+
+def conv_up(x: torch.Tensor, w: torch.Tensor, Ho: int, Wo: int, bias=None, act=ACT_NONE, out=None, ldo=None,
+            w3=None, b3=0.0, wpack=None, stream=None):
+    """3x3 conv of the align_corners=True resize of x (bf16 NHWC [B,Hs,Ws,Cp]) to Ho x Wo, fused.
+    With w3 ([32] f32): returns the DPT depth map relu(b3 + relu(conv + bias) . w3) [B,Ho,Wo] f32."""
+    B, Hs, Ws, Cp = x.shape
+    N = w.shape[0]
+    ldo = ldo or N
+    if wpack is None:
+        wpack = conv_up_pack(w, stream)
+    depth = None
+    if w3 is not None:
+        depth = out if out is not None else torch.empty(B, Ho, Wo, device=x.device)
+        out = None
+    elif out is None:
+        out = torch.zeros(B, Ho, Wo, ldo, device=x.device, dtype=torch.bfloat16)
+    check(lib.vpe_op_conv_up(_p(x), B, Hs, Ws, Cp, Ho, Wo, _p(wpack), N, _p(bias), _p(out), ldo, act, _p(w3), b3,
+                             _p(depth), _s(stream)), "vpe_op_conv_up")
+    return depth if w3 is not None else out
+
+
 def attention(qkv: torch.Tensor, B: int, T: int, D: int, heads: int, stream=None) -> torch.Tensor:
     out = torch.empty(B * T, D, device=qkv.device, dtype=torch.bfloat16)
     check(lib.vpe_op_attention(_p(qkv), _p(out), B, T, D, heads, _s(stream)), "vpe_op_attention")

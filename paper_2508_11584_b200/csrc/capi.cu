@@ -126,6 +126,38 @@ int vpe_op_conv(const void* x, int32_t B, int32_t H, int32_t W, int32_t C, int32
   return VPE_OK;
 }
 
+int vpe_op_conv_up_pack(const void* w, int32_t Cp, void* wpack, void* stream) {
+  if (!w || !wpack || (Cp != 32 && Cp != 64)) return VPE_E_VALUE;
+  VPE_TRY(pack_conv_up_weights(static_cast<const __nv_bfloat16*>(w), Cp, static_cast<__nv_bfloat16*>(wpack),
+                               static_cast<cudaStream_t>(stream)));
+  return VPE_OK;
+}
+
+int vpe_op_conv_up(const void* x, int32_t B, int32_t Hs, int32_t Ws, int32_t Cp, int32_t Ho, int32_t Wo,
+                   const void* wpack, int32_t N, const float* bias, void* out, int32_t ldo, int32_t act,
+                   const float* w3, float b3, float* depth, void* stream) {
+  if (!x || !wpack || B < 1 || (w3 ? (!depth || N != 32) : !out)) return VPE_E_VALUE;
+  EpiParams ep;
+  ep.kind = w3 ? EPI_DEPTH : EPI_CONV;
+  ep.act = act;
+  ep.N = N;
+  ep.bias = bias;
+  ep.out = out;
+  ep.ldo = ldo;
+  ep.w3 = w3;
+  ep.b3 = b3;
+  ep.max_depth = 1.f;
+  ep.depth = depth;
+  ep.depth_pre = depth;
+  GemmPlan g;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  VPE_TRY(plan_conv_up(&g, static_cast<const __nv_bfloat16*>(x), B, Hs, Ws, Cp, Ho, Wo, nullptr, N, ep,
+                       static_cast<__nv_bfloat16*>(const_cast<void*>(wpack)), s));
+  VPE_TRY(launch_gemm(g, s));
+  count_launches(1);
+  return VPE_OK;
+}
+
 int vpe_set_pdl(int32_t on) {
   pdl_flag() = on ? 1 : 0;
   return VPE_OK;

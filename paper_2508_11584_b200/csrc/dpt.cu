@@ -11,11 +11,15 @@
 //                   (both linear, weights sum to 1 -> identical math, 4x fewer FLOPs)
 //   head            conv1 3x3, bilinear to (14h,14w), conv2 3x3 with ReLU -> 1x1 -> ReLU*max_depth
 //                   fused into conv2's epilogue (depth written directly, pre-ReLU map optional).
-//                   Tried (round 1): building the two resizes inside the convs' halo producers
-//                   (8 CUDA-core warps interpolating from global) -- slower than resize kernel +
-//                   halo conv (head1 290 vs 215 us, head2 373 vs 350 us at B=16, ncu launch list)
+//                   Both head resizes are fused into the conv that consumes them (conv_up_kernel:
+//                   the halo is interpolated in smem from a TMA-staged source box, so the 2x and
+//                   14h-wide maps never reach HBM; bit-identical to resize + halo conv).
+//                   VPE_DPT_UNFUSED=1 restores the resize kernels (A/B). Round 1's attempt
+//                   interpolated from global memory inside the producer and lost to the resize
+//                   kernel + halo conv (head1 290 vs 215 us, head2 373 vs 350 us at B=16).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <new>
 
 #include "gemm.cuh"
@@ -42,6 +46,8 @@ struct vpe_dpt {
   const void* bound[4] = {nullptr};
   GemmPlan rs[4], rs3conv, neck[4], rcu[4][4], proj[4], head1;
   GemmPlan head2;  // epilogue pointers patched per call (depth outputs)
+  bool fused_up = false;  // head1 / head2 read the un-resized maps (conv_up_kernel)
+  bf16 *wpack1 = nullptr, *wpack2 = nullptr;  // their dy-stacked weights
   int nkern = 0;
 };
 
@@ -88,6 +94,8 @@ extern "C" int vpe_dpt_destroy(vpe_dpt* d) {
   cudaFree(d->h1);
   cudaFree(d->h1up);
   cudaFree(d->depth_pre_tmp);
+  cudaFree(d->wpack1);
+  cudaFree(d->wpack2);
   delete d;
   return VPE_OK;
 }
@@ -131,8 +139,7 @@ extern "C" int vpe_dpt_create(const vpe_dpt_config* cfg, const vpe_dpt_weights* 
   ok = ok && alloc(&d->t, big) && alloc(&d->hid, big) && alloc(&d->hidr, big) && alloc(&d->o, big) &&
        alloc(&d->po, big) && alloc(&d->fused, big);
   const int S4 = 2 * d->S[0];
-  ok = ok && alloc(&d->head_in, (size_t)B * S4 * S4 * F) && alloc(&d->h1, (size_t)B * S4 * S4 * d->Fh) &&
-       alloc(&d->h1up, (size_t)B * d->R * d->R * d->Fh);
+  ok = ok && alloc(&d->h1, (size_t)B * S4 * S4 * d->Fh);  // head_in / h1up: unfused path only
   ok = ok && cudaMalloc(&d->depth_pre_tmp, (size_t)B * d->R * d->R * 4) == cudaSuccess;
   if (!ok) return fail(VPE_E_RESOURCE);
   int rc;
@@ -176,7 +183,6 @@ extern "C" int vpe_dpt_create(const vpe_dpt_config* cfg, const vpe_dpt_weights* 
   }
   {
     EpiParams e = conv_ep(d->Fh, w->head1_b, d->h1, d->Fh, ACT_NONE, nullptr, nullptr, nullptr);
-    if ((rc = conv_plan(&d->head1, d->head_in, B, S4, F, w->head1_w, d->Fh, e))) return fail(rc);
     EpiParams e2;
     e2.kind = EPI_DEPTH;
     e2.N = d->Hh;
@@ -186,6 +192,21 @@ extern "C" int vpe_dpt_create(const vpe_dpt_config* cfg, const vpe_dpt_weights* 
     e2.max_depth = cfg->max_depth;
     e2.depth_pre = d->depth_pre_tmp;
     e2.depth = d->depth_pre_tmp;  // patched per call
+    const char* uf = getenv("VPE_DPT_UNFUSED");
+    d->fused_up = !(uf && uf[0] == '1') && F == 64 && d->Fh == 32 && d->Hh == 32 &&
+                  alloc(&d->wpack1, (size_t)3 * 96 * F) && alloc(&d->wpack2, (size_t)3 * 96 * d->Fh) &&
+                  plan_conv_up(&d->head1, d->po, B, d->S[0], d->S[0], F, S4, S4, static_cast<const bf16*>(w->head1_w),
+                               d->Fh, e, d->wpack1, 0) == VPE_OK &&
+                  plan_conv_up(&d->head2, d->h1, B, S4, S4, d->Fh, d->R, d->R, static_cast<const bf16*>(w->head2_w),
+                               d->Hh, e2, d->wpack2, 0) == VPE_OK &&
+                  cudaDeviceSynchronize() == cudaSuccess;
+    if (d->fused_up) {
+      *out = d;
+      return VPE_OK;
+    }
+    if (!alloc(&d->head_in, (size_t)B * S4 * S4 * F) || !alloc(&d->h1up, (size_t)B * d->R * d->R * d->Fh))
+      return fail(VPE_E_RESOURCE);
+    if ((rc = conv_plan(&d->head1, d->head_in, B, S4, F, w->head1_w, d->Fh, e))) return fail(rc);
     if ((rc = conv_plan(&d->head2, d->h1up, B, d->R, d->Fh, w->head2_w, d->Hh, e2))) return fail(rc);
   }
   *out = d;
@@ -249,17 +270,22 @@ extern "C" int vpe_dpt_forward(vpe_dpt* d, const void* const* taps, float* depth
       ++n;
     }
     VPE_TRY(launch_gemm(d->proj[k], s));
+    ++n;
+    if (k == 3 && d->fused_up) break;  // the x2 resize happens inside head1
     const int So = k < 3 ? d->S[fi - 1] : 2 * d->S[0];
     VPE_TRY(launch_bilinear_ac(d->po, B, S, S, F, k < 3 ? d->fused : d->head_in, So, So, F, s));
-    n += 2;
+    ++n;
   }
   VPE_TRY(launch_gemm(d->head1, s));
-  VPE_TRY(launch_bilinear_ac(d->h1, B, 2 * d->S[0], 2 * d->S[0], d->Fh, d->h1up, d->R, d->R, d->Fh, s));
+  if (!d->fused_up) {
+    VPE_TRY(launch_bilinear_ac(d->h1, B, 2 * d->S[0], 2 * d->S[0], d->Fh, d->h1up, d->R, d->R, d->Fh, s));
+    ++n;
+  }
   GemmPlan g2 = d->head2;
   g2.p.ep.depth = depth;
   g2.p.ep.depth_pre = depth_pre ? depth_pre : d->depth_pre_tmp;
   VPE_TRY(launch_gemm(g2, s));
-  n += 3;
+  n += 2;
   count_launches(n);
   return VPE_OK;
 }

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "bilerp.cuh"
 #include "gemm.cuh"
 #include "tc.cuh"
 #include "util.cuh"
@@ -69,6 +70,23 @@ VPE_DEV void load_bf16x32_add(const __nv_bfloat16* src, float (&v)[32]) {
   }
 }
 
+// Activation over a whole chunk behind one (warp-uniform) branch per kind: a per-element
+// apply_act() let the compiler if-convert the erf-GELU into every element's path (measured: the
+// predicated-off MUFU/FFMA sequence ran for ReLU / identity epilogues too).
+// (GELU here is an out-of-line call: no engine conv uses it, and inlined it costs every
+// ReLU / identity epilogue registers.)
+__device__ __noinline__ float gelu_erf_call(float x) { return gelu_erf(x); }
+template <int NV>
+VPE_DEV void apply_act_n(float* v, int act) {
+  if (act == ACT_RELU) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = fmaxf(v[j], 0.f);
+  } else if (act == ACT_GELU) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = gelu_erf_call(v[j]);
+  }
+}
+
 VPE_DEV float apply_act(float x, int act) {
   if (act == ACT_GELU) return gelu_erf(x);  // scalar path; the TMA-store epilogue uses gelu_poly32
   if (act == ACT_RELU) return fmaxf(x, 0.f);
@@ -110,6 +128,15 @@ VPE_DEV void mul_vec32(float (&v)[32], const float* __restrict__ vec, int col0, 
   }
 }
 
+// DPT head conv3 (1x1, 32 -> 1) on relu(conv2): b3 + sum_c relu(v_c) w3_c, as four interleaved
+// partial sums (a 32-long dependent FMA chain was the epilogue's latency). w3 may be global or smem.
+VPE_DEV float depth_dot(const float (&v)[32], const float* w3, float b3) {
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < 32; ++j) a[j & 3] = __fmaf_rn(fmaxf(v[j], 0.f), w3[j], a[j & 3]);
+  return b3 + ((a[0] + a[1]) + (a[2] + a[3]));
+}
+
 // Direct (non-TMA) epilogue for one thread: one output row (gpix), 32 consecutive columns.
 VPE_DEV void epilogue_direct(const EpiParams& ep, int64_t gpix, int col0, float (&v)[32]) {
   const int N = ep.N;
@@ -134,7 +161,7 @@ VPE_DEV void epilogue_direct(const EpiParams& ep, int64_t gpix, int col0, float 
         }
       }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], ep.act);
+      apply_act_n<32>(v, ep.act);
       if (full) {
         store_bf16x32(out, v);
       } else {
@@ -182,8 +209,7 @@ VPE_DEV void epilogue_direct(const EpiParams& ep, int64_t gpix, int col0, float 
     }
     case EPI_F32: {
       float* o = reinterpret_cast<float*>(ep.out) + gpix * ep.ldo + col0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = apply_act(v[j], ep.act);
+      apply_act_n<32>(v, ep.act);
       if (full) {
         float4* o4 = reinterpret_cast<float4*>(o);
 #pragma unroll
@@ -218,9 +244,7 @@ VPE_DEV void epilogue_direct(const EpiParams& ep, int64_t gpix, int col0, float 
       break;
     }
     case EPI_DEPTH: {
-      float pre = ep.b3;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) pre += fmaxf(v[j], 0.f) * __ldg(ep.w3 + j);
+      const float pre = depth_dot(v, ep.w3, ep.b3);
       ep.depth_pre[gpix] = pre;
       ep.depth[gpix] = fmaxf(pre, 0.f) * ep.max_depth;
       break;
@@ -286,8 +310,7 @@ VPE_DEV void epilogue_conv_staged(const EpiParams& ep, int64_t gpix, bool valid,
       }
       __syncwarp();
     }
-#pragma unroll
-    for (int j = 0; j < CH; ++j) vh[j] = apply_act(vh[j], ep.act);
+    apply_act_n<CH>(vh, ep.act);
 #pragma unroll
     for (int o = 0; o < 2; ++o) {
       if (!outs[o]) continue;  // warp-uniform
@@ -1114,6 +1137,395 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// Upsample-fused 3x3 conv (DPT head: conv1 after the last fusion stage's x2 resize, conv2 after
+// the resize to 14h x 14w). The resized map is never written to HBM: per tile, warp 0 TMA-loads
+// the small source box the tile's halo samples from (no swizzle, [rows][cols][C] bf16), eight
+// builder warps interpolate the (RT+2) x 130-pixel halo straight into the swizzled K-major layout
+// conv_halo_kernel gets from TMA (bilerp on f32x2, same rounding as bilinear_ac_rows_kernel, so
+// the tile is bit-identical to the resized tensor), and the MMA warp / eight epilogue warps run
+// the halo conv's schedule unchanged (weights resident, taps as descriptor start offsets).
+// Traffic per output row drops from (RT+2)/RT halo rows of the resized map to ~(RT+2)/RT x the
+// resize ratio of source rows, and the resize kernel's write + re-read of the large map goes.
+// 20 warps (640 threads, 96 registers): TMA, MMA, two epilogue warps per TMEM lane quadrant,
+// ten builders (520 / 1040 jobs per tile in 2 / 4 rounds)
+constexpr int UP_EPI_WARPS = 8;
+constexpr int UP_BUILD_WARPS = 10;
+constexpr int UP_THREADS = 32 * (2 + UP_EPI_WARPS + UP_BUILD_WARPS);
+constexpr int UP_MAX_SRC = 4;
+
+template <int BN, int KC, int RT>
+struct UpCfg {
+  static_assert(BN == 32, "conv_up_kernel: 32 output channels");
+  static constexpr int GCH = 8 * KC;   // channels (one group: Cp == GCH)
+  static constexpr int RB = 16 * KC;   // bytes per halo pixel
+  static constexpr int P = 130;        // halo pitch: 128 output pixels + 2
+  static constexpr uint32_t A_LAYOUT = KC == 8 ? 2 : 4;  // UMMA SWIZZLE_128B / SWIZZLE_64B
+  static constexpr int A_BYTES = (RB * P * (RT + 2) + 1023) / 1024 * 1024;
+  // dy-stacked weights: per dx one [96 = 3 x 32, GCH] K-major tile whose row block b holds the
+  // kernel row dy = 2 - b, so one N = 96 MMA on halo row h adds into the accumulators of output
+  // rows h-2, h-1, h, laid out 32 TMEM columns apart (see conv_up_kernel)
+  static constexpr int NS3 = 3 * BN;
+  static constexpr int B_BYTES = NS3 * GCH * 2;  // one dx tile
+  static constexpr int W_BYTES = (3 * B_BYTES + 1023) / 1024 * 1024;
+  static constexpr int B_SWZ = GCH == 64 ? 2 : 4;
+  static constexpr int B_SBO = 8 * GCH * 2;
+  static constexpr int AST = 2;        // halo stages
+  static constexpr int NACC = RT + 4;  // 32-column accumulators per tile: rows -2 .. RT+1
+  static constexpr int ACC = 2;        // tile accumulator sets in TMEM
+  static constexpr int TMEM_COLS = GemmCfg<NACC * BN, 64>::TMEM_COLS;
+  static constexpr int JOBS = P * KC;  // builder jobs per tile: (halo column, 16-byte channel chunk)
+  static constexpr size_t FIXED = 1024 + W_BYTES + AST * (size_t)A_BYTES + UP_EPI_WARPS * 2048 + 256;
+};
+
+// 8 channels: bf16x2 words unpacked to f32x2 (exact), bilerp as in bilerp() per lane
+VPE_DEV uint32_t bilerp_bf16x2(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint64_t hx, uint64_t lx, uint64_t hy,
+                               uint64_t ly) {
+  auto up = [](uint32_t w) {
+    return f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+  };
+  const uint64_t t0 = ffma2(lx, up(b), fmul2(hx, up(a)));
+  const uint64_t t1 = ffma2(lx, up(d), fmul2(hx, up(c)));
+  float r0, r1;
+  f2_unpack(ffma2(ly, t1, fmul2(hy, t0)), r0, r1);
+  return pack_bf16(r0, r1);
+}
+
+// diagnostics timeline (VPE_TRACE_BUILD + VPE_GEMM_TRACE=1): CTA 0, 500 events per role at
+// slots base.. (MMA 0, TMA 510, first builder warp 1020, first epilogue warp 1530)
+#ifdef VPE_TRACE_BUILD
+#define UP_TRACE(base, idx, code)                                                    \
+  do {                                                                               \
+    if (p.trace && blockIdx.x == 0 && (idx) < 500) {                                 \
+      g_gemm_trace[2 * ((base) + (idx))] = (unsigned long long)(code);               \
+      g_gemm_trace[2 * ((base) + (idx)) + 1] = (unsigned long long)clock64();        \
+      ++(idx);                                                                       \
+    }                                                                                \
+  } while (0)
+#else
+#define UP_TRACE(base, idx, code) \
+  do {                            \
+  } while (0)
+#endif
+
+template <int BN, int KC, int RT>
+__global__ void __launch_bounds__(UP_THREADS, 1)
+    conv_up_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tb,
+                   const GemmParams p) {
+  using C = UpCfg<BN, KC, RT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int NS = p.up_stages, SB = p.up_src_bytes;
+  uint8_t* sB = smem;
+  uint8_t* sA = sB + C::W_BYTES;
+  uint8_t* sS = sA + C::AST * C::A_BYTES;
+  uint8_t* sStg = sS + NS * SB;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sStg + UP_EPI_WARPS * 2048);
+  uint64_t* a_empty = a_full + C::AST;
+  uint64_t* s_full = a_empty + C::AST;
+  uint64_t* s_empty = s_full + UP_MAX_SRC;
+  uint64_t* w_full = s_empty + UP_MAX_SRC;
+  uint64_t* tfull = w_full + 1;
+  uint64_t* tempty = tfull + C::ACC;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + C::ACC);
+
+  __shared__ float s_bias[32], s_w3[32];  // epilogue constants (N <= 32), broadcast reads
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 2) {
+    s_bias[lane] = (p.ep.bias && (int)lane < p.ep.N) ? p.ep.bias[lane] : 0.f;
+    s_w3[lane] = p.ep.w3 ? p.ep.w3[lane] : 0.f;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&ts);
+    tma_prefetch(&tb);
+    for (int i = 0; i < C::AST; ++i) {
+      mbar_init(&a_full[i], UP_BUILD_WARPS);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < C::ACC; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], UP_EPI_WARPS);
+    }
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], UP_BUILD_WARPS);
+    }
+    mbar_init(w_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp >= 2 && warp < 2 + UP_EPI_WARPS) {  // every MMA accumulates: start from zero
+    float z[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) z[j] = 0.f;
+    for (int c = (warp - 2) >> 2; c < C::TMEM_COLS / 32; c += UP_EPI_WARPS / 4)
+      tmem_st32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + c * 32, z);
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_wait();
+  pdl_trigger();
+  const int ntiles = p.m_tiles;
+  const float sh = p.up_sh, sw = p.up_sw;
+  // tile t -> image, first output row, first output column; source box origin
+  auto tile_of = [&](int t, int& img, int& y0, int& x0) {
+    img = t / p.tiles_per_img;
+    const int rr = t - img * p.tiles_per_img;
+    y0 = (rr / p.tiles_x) * RT;
+    x0 = (rr - (rr / p.tiles_x) * p.tiles_x) * 128;
+  };
+  auto src_origin = [&](int y0, int x0, int& sy, int& sx) {
+    sy = ac_coord(sh, y0 > 0 ? y0 - 1 : 0, p.up_hs).i0;
+    sx = ac_coord(sw, x0 > 0 ? x0 - 1 : 0, p.up_ws).i0;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(w_full, 3 * C::B_BYTES);
+      for (int dx = 0; dx < 3; ++dx) tma_load_2d(sB + dx * C::B_BYTES, &tb, w_full, 0, dx * C::NS3);
+      int i = 0, tix = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int ss = i % NS;
+        mbar_wait_sleep(&s_empty[ss], ((i / NS) & 1) ^ 1);
+        UP_TRACE(510, tix, 11);
+        int img, y0, x0, sy, sx;
+        tile_of(t, img, y0, x0);
+        src_origin(y0, x0, sy, sx);
+        mbar_expect_tx(&s_full[ss], p.up_box_bytes);
+        tma_load_4d(sS + ss * SB, &ts, &s_full[ss], 0, sx, sy, img);
+      }
+    }
+  } else if (warp == 1) {
+    // the whole warp walks the loop (warp-voted waits keep descriptors in uniform registers);
+    // one elected lane issues
+    constexpr uint32_t idesc = idesc_bf16(128, C::NS3);
+    const uint64_t a_desc0 = smem_desc(smem_u32(sA), 16, 8 * C::RB, C::A_LAYOUT);
+    const uint64_t b_desc0 = smem_desc(smem_u32(sB), 16, C::B_SBO, C::B_SWZ);
+    const uint32_t a_lo0 = (uint32_t)a_desc0, a_hi = (uint32_t)(a_desc0 >> 32);
+    const uint32_t b_lo0 = (uint32_t)b_desc0, b_hi = (uint32_t)(b_desc0 >> 32);
+    mbar_wait_warp(w_full, 0);
+    tc_fence_after();
+    int i = 0, tix = 0;
+    const bool tr = lane == 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int acc = i % C::ACC, sa = i % C::AST;
+      mbar_wait_warp(&tempty[acc], ((i / C::ACC) & 1) ^ 1);
+      if (tr) UP_TRACE(0, tix, 1);
+      tc_fence_after();
+      mbar_wait_warp(&a_full[sa], (i / C::AST) & 1);
+      if (tr) UP_TRACE(0, tix, 2);
+      tc_fence_after();
+      const uint32_t d = tmem + acc * C::NACC * BN;
+      const uint32_t a_lo = a_lo0 + (uint32_t)sa * (C::A_BYTES >> 4);
+      // halo row h, shift dx: columns [h*32, h*32 + 96) = accumulators of output rows h-2..h
+#pragma unroll
+      for (int h = 0; h < ((p.dbg & 2) ? 0 : RT + 2); ++h) {
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const uint32_t at = a_lo + (uint32_t)(h * C::P + dx) * (C::RB / 16);
+          const uint32_t b_lo = b_lo0 + (uint32_t)(dx * (C::B_BYTES >> 4));
+#pragma unroll
+          for (int k = 0; k < KC / 2; ++k) {
+            const uint64_t ad = ((uint64_t)a_hi << 32) | (at + (uint32_t)k * 2u);
+            const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo + (uint32_t)(k * 2));
+            if (elect_one()) umma_f16(d + h * BN, ad, bd, idesc, 1u);
+          }
+        }
+      }
+      if (elect_one()) umma_commit(&a_empty[sa]);
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (tr) UP_TRACE(0, tix, 3);
+    }
+  } else if (warp < 2 + UP_EPI_WARPS) {
+    const int e = warp - 2, q = warp & 3, chalf = e >> 2;  // two warps per TMEM lane quadrant
+    const bool staged =
+        p.ep.kind == EPI_CONV && (p.ep.ldo & 7) == 0 &&
+        ((reinterpret_cast<uintptr_t>(p.ep.out) | reinterpret_cast<uintptr_t>(p.ep.out_relu) |
+          reinterpret_cast<uintptr_t>(p.ep.add1) | reinterpret_cast<uintptr_t>(p.ep.add2)) & 15) == 0;
+    uint8_t* stg = sStg + e * 2048;
+    const int r = q * 32 + lane;  // output pixel within the tile's 128-wide row
+    int i = 0, tix = 0;
+    const bool tr = e == 0 && lane == 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int acc = i % C::ACC;
+      int img, y0, x0;
+      tile_of(t, img, y0, x0);
+      mbar_wait_sleep(&tfull[acc], (i / C::ACC) & 1);
+      if (tr) UP_TRACE(1530, tix, 31);
+      tc_fence_after();
+      const uint32_t tbase = tmem + acc * C::NACC * BN + ((uint32_t)(q * 32) << 16);
+      float z[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) z[jj] = 0.f;
+      // rows -2, -1, RT, RT+1 collect the dy-stack's out-of-tile partial sums: clear them
+      for (int k = chalf; k < 4; k += UP_EPI_WARPS / 4) tmem_st32(tbase + (k < 2 ? k : RT + k) * BN, z);
+#pragma unroll 1
+      for (int k = chalf; k < RT; k += UP_EPI_WARPS / 4) {
+        const int rt = k, c0 = 0;
+        float v[32];
+        tmem_ld32(tbase + (rt + 2) * BN, v);
+        tmem_ld_wait();
+        tmem_st32(tbase + (rt + 2) * BN, z);
+        if (k + UP_EPI_WARPS / 4 >= RT) {  // last TMEM access of the tile by this warp
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        const int y = y0 + rt, x = x0 + r;
+        const bool valid = y < p.H && x < p.W;
+        const int64_t gpix = ((int64_t)img * p.H + y) * p.W + x;
+        if (p.ep.kind == EPI_DEPTH) {  // N == 32: bias and w3 from smem
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) v[jj] += s_bias[jj];
+          const float pre = depth_dot(v, s_w3, p.ep.b3);
+          if (valid) {
+            p.ep.depth_pre[gpix] = pre;
+            p.ep.depth[gpix] = fmaxf(pre, 0.f) * p.ep.max_depth;
+          }
+        } else if (staged && c0 + 32 <= p.ep.N) {
+          epilogue_conv_staged<4>(p.ep, gpix, valid, c0, v, stg);
+        } else if (valid && c0 < p.ep.N) {
+          epilogue_direct(p.ep, gpix, c0, v);
+        }
+      }
+      if (tr) UP_TRACE(1530, tix, 32);
+    }
+  } else {
+    // builders. Job = (halo column c, 16-byte channel chunk g) for all RT+2 halo rows: the
+    // horizontal lerp t = lx*b + hx*a of a source row is computed once and kept while consecutive
+    // halo rows sample that row (ratio < 1: a source row serves ~1/ratio halo rows), then
+    // out = ly*t(i1) + hy*t(i0) -- bilerp()'s exact operation order, on f32x2. Rows are the outer
+    // loop (their sampling is tile-uniform: no divergence) and each thread carries two jobs
+    // through it side by side, so the two dependent LDS -> FMA -> STS chains overlap.
+    constexpr int NB = UP_BUILD_WARPS * 32;
+    const int bt = (int)(warp - 2 - UP_EPI_WARPS) * 32 + (int)lane;
+    const int row_bytes = p.up_cols * C::GCH * 2;
+    int i = 0, tix = 0;
+    const bool tr = bt == 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int sa = i % C::AST, ss = i % NS;
+      int img, y0, x0, sy, sx;
+      tile_of(t, img, y0, x0);
+      src_origin(y0, x0, sy, sx);
+      mbar_wait_sleep(&a_empty[sa], ((i / C::AST) & 1) ^ 1);
+      if (tr) UP_TRACE(1020, tix, 21);
+      mbar_wait_sleep(&s_full[ss], (i / NS) & 1);
+      if (tr) UP_TRACE(1020, tix, 22);
+      const uint32_t src = smem_u32(sS + ss * SB);
+      const uint32_t dst = smem_u32(sA + sa * C::A_BYTES);
+#pragma unroll 1
+      for (int jb = ((p.dbg & 1) ? C::JOBS : bt); jb < C::JOBS; jb += 2 * NB) {
+        uint32_t s0[2], s1[2];
+        uint64_t hx[2], lx[2], hl[2][4], hh[2][4];
+        int cj[2], gj[2];
+        bool xv[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int j = jb + q * NB < C::JOBS ? jb + q * NB : jb;  // a missing second job redoes the first
+          cj[q] = j / KC;
+          gj[q] = j - cj[q] * KC;
+          const int X = x0 - 1 + cj[q];
+          xv[q] = X >= 0 && X < p.W;  // lane-dependent: applied as a select at the store
+          const AcCoord cx = ac_coord(sw, xv[q] ? X : 0, p.up_ws);
+          s0[q] = src + ((cx.i0 - sx) * C::GCH + gj[q] * 8) * 2;
+          s1[q] = src + ((cx.i1 - sx) * C::GCH + gj[q] * 8) * 2;
+          hx[q] = f2_pack(cx.h, cx.h);
+          lx[q] = f2_pack(cx.l, cx.l);
+        }
+        auto hlerp = [&](int q, int roff, uint64_t (&h)[4]) {
+          const uint4 a = lds128(s0[q] + roff);
+          const uint4 b = lds128(s1[q] + roff);
+          const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t av = f2_pack(__uint_as_float(aw[k] << 16), __uint_as_float(aw[k] & 0xffff0000u));
+            const uint64_t bv = f2_pack(__uint_as_float(bw[k] << 16), __uint_as_float(bw[k] & 0xffff0000u));
+            h[k] = ffma2(lx[q], bv, fmul2(hx[q], av));
+          }
+        };
+        int cur0 = -1, cur1 = -1;  // source rows (byte offsets) held in hl / hh: tile-uniform
+#pragma unroll
+        for (int r = 0; r < RT + 2; ++r) {
+          const int Y = y0 - 1 + r;
+          uint32_t o[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int px = r * C::P + cj[q];
+            const int swz = KC == 8 ? (px & 7) : ((px >> 1) & 3);  // TMA/UMMA 128B / 64B swizzle
+            o[q] = dst + px * C::RB + ((gj[q] ^ swz) << 4);
+          }
+          if (Y < 0 || Y >= p.H) {
+            sts128(o[0], make_uint4(0, 0, 0, 0));
+            sts128(o[1], make_uint4(0, 0, 0, 0));
+            continue;
+          }
+          const AcCoord cy = ac_coord(sh, Y, p.up_hs);
+          const int n0 = (cy.i0 - sy) * row_bytes, n1 = (cy.i1 - sy) * row_bytes;
+          if (n0 != cur0) {
+            if (n0 == cur1) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                hl[0][k] = hh[0][k];
+                hl[1][k] = hh[1][k];
+              }
+            } else {
+              hlerp(0, n0, hl[0]);
+              hlerp(1, n0, hl[1]);
+            }
+            cur0 = n0;
+          }
+          if (n1 != cur1) {
+            if (n1 == cur0) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                hh[0][k] = hl[0][k];
+                hh[1][k] = hl[1][k];
+              }
+            } else {
+              hlerp(0, n1, hh[0]);
+              hlerp(1, n1, hh[1]);
+            }
+            cur1 = n1;
+          }
+          const uint64_t hy = f2_pack(cy.h, cy.h), ly = f2_pack(cy.l, cy.l);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              float v0, v1;
+              f2_unpack(ffma2(ly, hh[q][k], fmul2(hy, hl[q][k])), v0, v1);
+              w[k] = xv[q] ? pack_bf16(v0, v1) : 0u;
+            }
+            sts128(o[q], make_uint4(w[0], w[1], w[2], w[3]));
+          }
+        }
+      }
+      fence_async_smem();  // generic-proxy halo writes -> tensor-core (async proxy) reads
+      __syncwarp();
+      if (tr) UP_TRACE(1020, tix, 23);
+      if (lane == 0) {
+        mbar_arrive(&a_full[sa]);
+        mbar_arrive(&s_empty[ss]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1356,6 +1768,112 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   return VPE_OK;
 }
 
+int pack_conv_up_weights(const __nv_bfloat16* B, int Cp, __nv_bfloat16* wpack, cudaStream_t stream) {
+  // dy-stacked weights: wpack[dx][b * 32 + co][c] = W[co][tap (2 - b, dx)][c] (UpCfg)
+  for (int dx = 0; dx < 3; ++dx)
+    for (int b = 0; b < 3; ++b)
+      VPE_CUDA_TRY(cudaMemcpy2DAsync(wpack + (size_t)(dx * 96 + b * 32) * Cp, (size_t)Cp * 2,
+                                     B + (size_t)((2 - b) * 3 + dx) * Cp, (size_t)9 * Cp * 2, (size_t)Cp * 2, 32,
+                                     cudaMemcpyDeviceToDevice, stream));
+  return VPE_OK;
+}
+
+int plan_conv_up(GemmPlan* g, const __nv_bfloat16* X, int nimg, int Hs, int Ws, int Cp, int Ho, int Wo,
+                 const __nv_bfloat16* B, int N, const EpiParams& ep, __nv_bfloat16* wpack, cudaStream_t stream) {
+  if ((Cp != 32 && Cp != 64) || N != 32 || Wo < 128 || Ho < 2 || Hs < 1 || Ws < 1 || !wpack) return VPE_E_SHAPE;
+  if (reinterpret_cast<uintptr_t>(X) % 16 || reinterpret_cast<uintptr_t>(B) % 16 ||
+      reinterpret_cast<uintptr_t>(wpack) % 16)  // B null: wpack already holds the packed weights
+    return VPE_E_SHAPE;
+  const int kc = Cp / 8, rt = Cp == 32 ? 4 : 2, bn = 32;
+  memset(g, 0, sizeof(*g));
+  const float sh = ac_scale(Hs, Ho), sw = ac_scale(Ws, Wo);
+  // source box: the largest span any tile's halo samples (same float math as the kernel)
+  auto span = [](float s, int n_in, int n_out, int step, int len) {
+    int m = 0;
+    for (int o0 = 0; o0 < n_out; o0 += step) {
+      const int lo = o0 > 0 ? o0 - 1 : 0, hi = o0 + len < n_out ? o0 + len : n_out - 1;
+      const int i_lo = ac_i0_host(s, lo), i_hi0 = ac_i0_host(s, hi);
+      const int i_hi = i_hi0 + (i_hi0 < n_in - 1);
+      if (i_hi - i_lo + 1 > m) m = i_hi - i_lo + 1;
+    }
+    return m;
+  };
+  const int rows = span(sh, Hs, Ho, rt, rt), cols = span(sw, Ws, Wo, 128, 128);
+  if (rows > 256 || cols > 256) return VPE_E_SHAPE;
+  {
+    uint64_t dims[4] = {(uint64_t)Cp, (uint64_t)Ws, (uint64_t)Hs, (uint64_t)nimg};
+    uint64_t strides[3] = {(uint64_t)Cp * 2, (uint64_t)Ws * Cp * 2, (uint64_t)Hs * Ws * Cp * 2};
+    uint32_t box[4] = {(uint32_t)Cp, (uint32_t)cols, (uint32_t)rows, 1u};
+    VPE_TRY(encode_tma(&g->ta, 4, X, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE));
+  }
+  if (B) VPE_TRY(pack_conv_up_weights(B, Cp, wpack, stream));
+  {
+    uint64_t dims[2] = {(uint64_t)Cp, 288};
+    uint64_t strides[1] = {(uint64_t)Cp * 2};
+    uint32_t box[2] = {(uint32_t)Cp, 96};
+    VPE_TRY(encode_tma(&g->tb, 2, wpack, dims, strides, box,
+                       Cp == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B));
+  }
+  const int box_bytes = rows * cols * Cp * 2;
+  const int src_bytes = (box_bytes + 127) / 128 * 128;
+  const size_t fixed = Cp == 32 ? UpCfg<32, 4, 4>::FIXED : UpCfg<32, 8, 2>::FIXED;
+  const size_t budget = 227 * 1024 - 512;  // dynamic + the kernel's static epilogue constants
+  int stages = 0;
+  while (stages < UP_MAX_SRC && fixed + (size_t)(stages + 1) * src_bytes <= budget) ++stages;
+  if (stages < 1) return VPE_E_SHAPE;
+  static const int max_st = getenv("VPE_UP_STAGES") ? atoi(getenv("VPE_UP_STAGES")) : UP_MAX_SRC;
+  if (max_st >= 1 && stages > max_st) stages = max_st;
+  g->p.mode = 3;
+  g->p.kcp = Cp;
+  g->p.cchunks = 1;
+  g->p.ks = 3;
+  g->p.H = Ho;
+  g->p.W = Wo;
+  g->p.bw = 128;
+  g->p.bh = rt;
+  g->p.hp = 130;
+  g->p.tiles_x = (Wo + 127) / 128;
+  g->p.tiles_per_img = g->p.tiles_x * ((Ho + rt - 1) / rt);
+  g->p.M = nimg * Ho * Wo;
+  g->p.up_hs = Hs;
+  g->p.up_ws = Ws;
+  g->p.up_rows = rows;
+  g->p.up_cols = cols;
+  g->p.up_stages = stages;
+  g->p.up_src_bytes = src_bytes;
+  g->p.up_box_bytes = box_bytes;
+  g->p.up_sh = sh;
+  g->p.up_sw = sw;
+  g->p.ep = ep;
+  finish_grid(g, N, bn, nimg * g->p.tiles_per_img);
+  g->bn = bn;
+  g->bk = Cp;
+  g->up_kc = kc;
+  g->halo_rt = rt;
+  g->smem = fixed + (size_t)stages * src_bytes;
+  return VPE_OK;
+}
+
+template <int BN, int KC, int RT>
+static int launch_up_t(const GemmPlan& g, cudaStream_t s) {
+  auto k = conv_up_kernel<BN, KC, RT>;
+  static OncePerDevice attr_set;
+  if (attr_set.first()) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 512);
+    max_smem_carveout(k);
+  }
+  PdlKind pk(8);
+  static const int dbg = getenv("VPE_UP_DBG") ? atoi(getenv("VPE_UP_DBG")) : 0;  // 1 no build, 2 no MMA
+  GemmParams p = g.p;
+  p.dbg = dbg;
+  if (g_gemm_trace_on < 0) {
+    const char* e = getenv("VPE_GEMM_TRACE");
+    g_gemm_trace_on = (e && e[0] == '1') ? 1 : 0;
+  }
+  p.trace = g_gemm_trace_on;
+  return launch_k(k, g.grid, dim3(UP_THREADS), g.smem, s, g.ta, g.tb, p) == cudaSuccess ? VPE_OK : VPE_E_CUDA;
+}
+
 template <int BN, int KC, int RT, bool WRES = false>
 static int launch_halo_t(const GemmPlan& g0, cudaStream_t s) {
   auto k = conv_halo_kernel<BN, KC, RT, WRES>;
@@ -1474,6 +1992,9 @@ int launch_gemm_resid_ln(const GemmPlan& g0, __nv_bfloat16* xln, __nv_bfloat16* 
 
 int launch_gemm(const GemmPlan& g, cudaStream_t s) {
   if (g.resid_ln) return launch_gemm_resid_ln(g, nullptr, nullptr, s);
+  if (g.up_kc == 4 && g.halo_rt == 4 && g.bn == 32) return launch_up_t<32, 4, 4>(g, s);
+  if (g.up_kc == 8 && g.halo_rt == 2 && g.bn == 32) return launch_up_t<32, 8, 2>(g, s);
+  if (g.up_kc) return VPE_E_SHAPE;
   if (g.halo_kc) {
 #define VPE_LH(BN_, KC_, RT_)                                                         \
   if (g.bn == BN_ && g.halo_kc == KC_ && g.halo_rt == RT_)                            \

@@ -69,6 +69,9 @@ struct GemmParams {
   int tma_out = 0;               // 1: epilogue leaves through TMA store / reduce-add (tout)
   int hp = 0, rows_box = 0;      // halo conv: virtual row pitch P, halo rows per stage
   int parts = 1, kcp = 0;        // halo conv: split-precision weight parts, K extent per tap (Cpad)
+  // upsample-fused conv (conv_up_kernel): source map Hs x Ws, align_corners scales, source box
+  int up_hs = 0, up_ws = 0, up_rows = 0, up_cols = 0, up_stages = 0, up_src_bytes = 0, up_box_bytes = 0;
+  float up_sh = 0.f, up_sw = 0.f;
   int trace = 0;                 // diagnostics: record the MMA timeline of CTA 0
   int dbg = 0;                   // diagnostics (halo conv, VPE_HALO_DBG): 1 no stores, 2 no A reloads, 4 no MMA
   EpiParams ep;
@@ -85,6 +88,7 @@ struct GemmPlan {
   int halo_kc = 0;  // > 0: conv_halo_kernel<bn, halo_kc, halo_rt>
   int halo_rt = 1;
   int halo_wres = 0;  // 1: conv_halo_kernel<.., WRES> (all weight tiles resident in smem)
+  int up_kc = 0;      // > 0: conv_up_kernel<bn, up_kc, halo_rt> (resize fused into the halo builder)
   int resid_ln = 0; // 1: gemm_resid_ln_kernel (residual GEMM + the next LayerNorm in the epilogue)
   CUtensorMap tx;   // resid_ln: bf16 LayerNorm output map
   size_t smem = 0;
@@ -97,6 +101,16 @@ struct GemmPlan {
 int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, int Cp, int64_t pitch_px,
                    int64_t pitch_row, int64_t pitch_img, int parts, const __nv_bfloat16* B, int N, int64_t ldb,
                    const EpiParams& ep, int bn);
+
+// 3x3 / stride 1 / pad 1 conv of the align_corners=True bilinear resize of X (NHWC [nimg, Hs, Ws,
+// Cp], Cp = 32 or 64, dense) to Ho x Wo (Wo >= 128), without materialising the resized map: the
+// halo tiles are interpolated in shared memory from TMA-staged source boxes. Bit-identical to
+// launch_bilinear_ac followed by the same conv. Weights [N = 32, 9*Cp] tap-major, repacked
+// (stream-ordered) into wpack (3 * 96 * Cp bf16, caller-owned, kept for the plan's lifetime);
+// B null: wpack was packed already (pack_conv_up_weights).
+int pack_conv_up_weights(const __nv_bfloat16* B, int Cp, __nv_bfloat16* wpack, cudaStream_t stream);
+int plan_conv_up(GemmPlan* g, const __nv_bfloat16* X, int nimg, int Hs, int Ws, int Cp, int Ho, int Wo,
+                 const __nv_bfloat16* B, int N, const EpiParams& ep, __nv_bfloat16* wpack, cudaStream_t stream);
 
 // --- host-side builders (gemm.cu) ---
 bool tma_available();

@@ -7,6 +7,7 @@
 
 #include <cstdlib>
 
+#include "bilerp.cuh"
 #include "ln.cuh"
 #include "misc.cuh"
 #include "tc.cuh"
@@ -234,15 +235,6 @@ int launch_layernorm(const float* x, int M, int D, const float* w, const float* 
 }
 
 // ---------------------------------------------------------------------------------------------
-// hy*(hx*a + lx*b) + ly*(hx*c + lx*d) with the FMA contraction spelled out, so that every resize
-// variant below rounds identically (bit-identical outputs whichever kernel the shape selects)
-__device__ __forceinline__ float bilerp(float a, float b, float c, float d, float hx, float lx, float hy, float ly) {
-  const float t0 = __fmaf_rn(lx, b, __fmul_rn(hx, a));
-  const float t1 = __fmaf_rn(lx, d, __fmul_rn(hx, c));
-  return __fmaf_rn(ly, t1, __fmul_rn(hy, t0));
-}
-
-// ---------------------------------------------------------------------------------------------
 // Bilinear resize on NHWC bf16, align_corners=True (modeling_depth_anything.py:157-200, 288-293).
 // Thread = up to 32 channels (4 x 16 B) of one output pixel: the bilinear weights are computed
 // once and 16 independent 16-byte loads are in flight per thread. Channel pitch cp, C real.
@@ -262,13 +254,9 @@ __global__ void __launch_bounds__(256) bilinear_ac_kernel(const __nv_bfloat16* _
   pix /= Wo;
   const int oy = pix % Ho;
   const int b = pix / Ho;
-  const float sh = Ho > 1 ? (float)(Hi - 1) / (float)(Ho - 1) : 0.f;
-  const float sw = Wo > 1 ? (float)(Wi - 1) / (float)(Wo - 1) : 0.f;
-  const float fy = sh * oy, fx = sw * ox;
-  const int y0 = (int)fy, x0 = (int)fx;
-  const int y1 = y0 + (y0 < Hi - 1), x1 = x0 + (x0 < Wi - 1);
-  const float ly = fy - y0, lx = fx - x0;
-  const float hy = 1.f - ly, hx = 1.f - lx;
+  const AcCoord cy = ac_coord(ac_scale(Hi, Ho), oy, Hi), cx = ac_coord(ac_scale(Wi, Wo), ox, Wi);
+  const int y0 = cy.i0, y1 = cy.i1, x0 = cx.i0, x1 = cx.i1;
+  const float ly = cy.l, hy = cy.h, lx = cx.l, hx = cx.h;
   const __nv_bfloat16* base = in + (int64_t)b * Hi * Wi * cp + g * 8 * NV;
   const uint4* p00 = reinterpret_cast<const uint4*>(base + ((int64_t)y0 * Wi + x0) * cp);
   const uint4* p01 = reinterpret_cast<const uint4*>(base + ((int64_t)y0 * Wi + x1) * cp);
@@ -312,12 +300,10 @@ __global__ void __launch_bounds__(256) bilinear_ac_rows_kernel(const __nv_bfloat
                                                                int Wo, int C) {
   extern __shared__ __align__(16) uint8_t s_rows[];  // [2][Wi][cp] bf16
   const int oy = blockIdx.x, b = blockIdx.y;
-  const float sh = Ho > 1 ? (float)(Hi - 1) / (float)(Ho - 1) : 0.f;
-  const float sw = Wo > 1 ? (float)(Wi - 1) / (float)(Wo - 1) : 0.f;
-  const float fy = sh * oy;
-  const int y0 = (int)fy;
-  const int y1 = y0 + (y0 < Hi - 1);
-  const float ly = fy - y0, hy = 1.f - ly;
+  const float sw = ac_scale(Wi, Wo);
+  const AcCoord cy = ac_coord(ac_scale(Hi, Ho), oy, Hi);
+  const int y0 = cy.i0, y1 = cy.i1;
+  const float ly = cy.l, hy = cy.h;
   const int row_vec = Wi * cp / 8;  // uint4 per source row
   const uint4* src0 = reinterpret_cast<const uint4*>(in + ((int64_t)b * Hi + y0) * Wi * cp);
   const uint4* src1 = reinterpret_cast<const uint4*>(in + ((int64_t)b * Hi + y1) * Wi * cp);
@@ -332,10 +318,9 @@ __global__ void __launch_bounds__(256) bilinear_ac_rows_kernel(const __nv_bfloat
   uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)b * Ho + oy) * Wo * cp);
   for (int t = threadIdx.x; t < Wo * groups; t += blockDim.x) {
     const int ox = t / groups, g = t - ox * groups;
-    const float fx = sw * ox;
-    const int x0 = (int)fx;
-    const int x1 = x0 + (x0 < Wi - 1);
-    const float lx = fx - x0, hx = 1.f - lx;
+    const AcCoord cx = ac_coord(sw, ox, Wi);
+    const int x0 = cx.i0, x1 = cx.i1;
+    const float lx = cx.l, hx = cx.h;
     const uint4 a = r0[(x0 * cp) / 8 + g], bq = r0[(x1 * cp) / 8 + g];
     const uint4 c = r1[(x0 * cp) / 8 + g], d = r1[(x1 * cp) / 8 + g];
     const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);

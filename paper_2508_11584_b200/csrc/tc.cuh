@@ -388,6 +388,18 @@ VPE_DEV void gelu_poly32(float (&v)[32]) {
   for (int j = 0; j < 16; ++j) f2_unpack(gelu_poly2(f2_pack(v[2 * j], v[2 * j + 1])), v[2 * j], v[2 * j + 1]);
 }
 
+// explicit shared-space 16-byte accesses (generic pointers into dynamic smem can compile to
+// LD.E / ST.E, which go through the generic address path)
+VPE_DEV uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+VPE_DEV void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
 VPE_DEV uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);

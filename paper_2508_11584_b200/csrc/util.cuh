@@ -107,6 +107,10 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess)
+    fprintf(stderr, "[vpe] launch failed: %s (grid %u, block %u, smem %zu)\n", cudaGetErrorString(e), grid.x, block.x,
+            smem);
+  return e;
 }
 }  // namespace vpe

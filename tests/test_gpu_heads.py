@@ -60,6 +60,25 @@ def test_depth_stagewise(setup):
     assert e <= 1e-2 and c >= 0.999
 
 
+
+def test_depth_fused_resize_bitexact(setup, monkeypatch):
+    """The DPT head with both resizes fused into their convs (default) writes exactly the depth the
+    unfused path (VPE_DPT_UNFUSED=1: resize kernels + halo convs) writes."""
+    from paper_2508_11584_b200.heads import DepthHead
+    s = setup
+    R, B, dev = s["R"], s["B"], s["dev"]
+    outs = []
+    for unfused in ("0", "1"):
+        monkeypatch.setenv("VPE_DPT_UNFUSED", unfused)
+        head = DepthHead(s["W"], s["cfg"], R, B, dev)
+        depth = torch.empty(B, R, R, device=dev)
+        pre = torch.empty(B, R, R, device=dev)
+        head.forward(s["taps"], depth, pre)
+        torch.cuda.synchronize()
+        outs.append((depth.clone(), pre.clone()))
+        del head
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
 def test_seg_stagewise(setup):
     from paper_2508_11584_b200.heads import SegHead
     s = setup

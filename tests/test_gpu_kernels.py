@@ -161,6 +161,34 @@ def test_bilinear_align_corners(ops, device, Hi, Ho, C):
     assert (err <= ref.abs() * 2 ** -7 + 1e-6).all(), err.max().item()
 
 
+@pytest.mark.parametrize("B,Hs,Ws,Cp,Ho,Wo", [(2, 128, 128, 64, 256, 256), (2, 256, 256, 32, 448, 448),
+                                             (16, 128, 128, 64, 256, 256), (1, 50, 61, 32, 130, 200),
+                                             (1, 37, 37, 64, 148, 148), (3, 64, 64, 32, 518, 300)])
+def test_conv_up_fused(ops, device, B, Hs, Ws, Cp, Ho, Wo):
+    """DPT head conv of the align_corners resize (conv_up_kernel, the resized map built in smem)
+    == the standalone resize kernel followed by the halo conv, bit for bit; and vs torch fp32."""
+    g = torch.Generator().manual_seed(Hs * 7 + Ho)
+    N = 32
+    x = torch.randn(B, Hs, Ws, Cp, generator=g).to(device, torch.bfloat16)
+    w = (torch.randn(N, 3, 3, Cp, generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(N, generator=g).to(device)
+    wk = w.reshape(N, -1).to(device)
+    fused = ops.conv_up(x, wk, Ho, Wo, bias=bias, act=ops.ACT_RELU)
+    up = ops.bilinear(x, Ho, Wo)
+    two = ops.conv(up, wk, Cp, 3, bias=bias, act=ops.ACT_RELU)
+    torch.cuda.synchronize()
+    assert torch.equal(fused, two), (fused.float() - two.float()).abs().max().item()
+    ref = F.interpolate(x.float().permute(0, 3, 1, 2), size=(Ho, Wo), mode="bilinear", align_corners=True)
+    ref = F.relu(F.conv2d(ref, w.float().permute(0, 3, 1, 2).to(device), bias, padding=1)).permute(0, 2, 3, 1)
+    assert rel_l2(fused, ref) < 8e-3
+    # DPT depth epilogue (head2 form): relu(b3 + relu(conv + bias) . w3), f32 out
+    w3 = torch.randn(N, generator=g).to(device) * 0.2
+    depth = ops.conv_up(x, wk, Ho, Wo, bias=bias, w3=w3, b3=0.05)
+    torch.cuda.synchronize()
+    ref_d = F.relu(two.float() @ w3 * 0 + (F.relu(ref) @ w3) + 0.05)  # ref already relu'd
+    assert rel_l2(depth, ref_d) < 1e-2
+
+
 @pytest.mark.parametrize("M,K,tap", [(16400, 384, False), (16400, 1536, True), (1025, 384, True), (300, 1536, False)])
 def test_linear_resid_ln(ops, device, M, K, tap):
     """Residual GEMM with the next LayerNorm in its epilogue vs the unfused pair (TMA reduce-add
