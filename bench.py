@@ -350,26 +350,36 @@ def kernel_rooflines(eng, peaks):
             # the same kernel against HBM: A, W, old + new fp32 residual, bf16 LN output
             out[-1]["hbm_bytes"] = M * K * 2 + D * K * 2 + M * D * (4 + 4 + 2)
             out[-1]["hbm_frac"] = out[-1]["hbm_bytes"] / (out[-1]["duration_us"] * 1e-6) / 1e9 / peaks["hbm"]
-    # DPT head: conv2 (3x3, Fh -> 32 at R x R, depth epilogue fused in the engine; plain conv here)
+    # DPT head (the engine's kernels): conv1 of the x2 resize and conv2 of the resize to R x R, each
+    # with the resize built in shared memory (conv_up_kernel), conv2 with the fused 1x1 + ReLU depth
+    # epilogue; algorithmic work = the two 3x3 convolutions at their output resolution
     F = eng.cfg.dpt.fusion
     Fh = F // 2
-    x = rnd(B, R, R, Fh)
-    w = rnd(32, 9 * Fh, std=0.05)
-    bias = torch.zeros(32, device=dev)
-    o = torch.empty(B, R, R, 32, device=dev, dtype=torch.bfloat16)
-    tensor("dpt_head_conv", "conv_halo_kernel<32,4,4,1>", {"B": B, "H": R, "C": Fh, "N": 32},
-           2.0 * B * R * R * 32 * 9 * Fh, lambda: _ops.conv(x, w, Fh, 3, bias=bias, out=o))
     S = 4 * (R // 14)
+    if F == 64:
+        po = rnd(B, S, S, F)
+        w1 = rnd(Fh, 9 * F, std=0.05)
+        w1p = _ops.conv_up_pack(w1)
+        b1 = torch.zeros(Fh, device=dev)
+        o1 = torch.empty(B, 2 * S, 2 * S, Fh, device=dev, dtype=torch.bfloat16)
+        tensor("dpt_head1_conv_up", "conv_up_kernel<32,8,2>", {"B": B, "Hs": S, "Ho": 2 * S, "C": F, "N": Fh},
+               2.0 * B * (2 * S) ** 2 * Fh * 9 * F,
+               lambda: _ops.conv_up(po, w1, 2 * S, 2 * S, bias=b1, out=o1, wpack=w1p))
+        h1 = rnd(B, 2 * S, 2 * S, Fh)
+        w2 = rnd(32, 9 * Fh, std=0.05)
+        w2p = _ops.conv_up_pack(w2)
+        b2 = torch.zeros(32, device=dev)
+        w3 = torch.randn(32, generator=g).to(dev) * 0.1
+        dep = torch.empty(B, R, R, device=dev)
+        tensor("dpt_head2_conv_up", "conv_up_kernel<32,4,4> +depth", {"B": B, "Hs": 2 * S, "Ho": R, "C": Fh, "N": 32},
+               2.0 * B * R * R * 32 * 9 * Fh,
+               lambda: _ops.conv_up(h1, w2, R, R, bias=b2, w3=w3, b3=0.1, out=dep, wpack=w2p))
     x2 = rnd(B, S, S, F)
     w2 = rnd(F, 9 * F, std=0.05)
     b2 = torch.zeros(F, device=dev)
     o2 = torch.empty(B, S, S, F, device=dev, dtype=torch.bfloat16)
     tensor("dpt_rcu_conv", "conv_halo_kernel<64,8,2,1>", {"B": B, "H": S, "C": F, "N": F},
            2.0 * B * S * S * F * 9 * F, lambda: _ops.conv(x2, w2, F, 3, bias=b2, out=o2))
-    # DPT resize 2S -> R (align_corners=True), Fh channels: read the source once, write the output
-    src = rnd(B, 2 * S, 2 * S, Fh)
-    hbm("dpt_bilinear", "bilinear_ac_rows_kernel", {"B": B, "Hi": 2 * S, "Ho": R, "C": Fh},
-        B * (2 * S * 2 * S + R * R) * Fh * 2, lambda: _ops.bilinear(src, R, R))
     # seg: fused upsample + argmax, logits read once, u8 labels written
     h = R // 14
     C = eng.cfg.seg_classes
