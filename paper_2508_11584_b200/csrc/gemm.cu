@@ -944,15 +944,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  pdl_wait();
-  pdl_trigger();
   const int ntiles = p.m_tiles * p.n_tiles;
   const int groups = p.cchunks;  // channel groups of GCH
+  // dy-stacked MMAs (RT >= 2 output rows on one halo, weights resident, one part / group): the
+  // three kernel rows of a tap column sit as one [dy2; dy1; dy0] x BN tile, so a single MMA on
+  // halo row h (N = 64 / 128 / .. BN-blocks) adds into the accumulators of every output row it
+  // touches (rows h-2..h, BN TMEM columns apart): (RT+2) x 3 x KC/2 MMAs per tile instead of
+  // 9 x RT x KC/2, the A operand read once per halo row instead of once per (row, dy). Same
+  // per-row accumulation order as the tap loop (dy-major, dx, k). Every MMA accumulates, so the
+  // epilogue zeroes each accumulator chunk after reading it (and all of TMEM starts at zero).
+  const bool dys = RT >= 2 && WRES && p.parts == 1 && groups == 1;
+  if (dys && warp >= 2) {
+    const int e = warp - 2;
+    for (int c = e >> 2; c < C::TMEM_COLS / 32; c += EPI_SPLIT)
+      tmem_zero32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + c * 32);
+    tmem_st_wait();
+  }
+  if (dys) {
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
       int ia = 0, ib = 0;
-      if (WRES) {  // all weight tiles once (single N tile: the planner guarantees n_tiles == 1)
+      if (WRES && dys) {  // tap (dy, dx) -> rows (2 - dy) * BN of the dx tile [dy2; dy1; dy0]
+        mbar_expect_tx(&b_full[0], 9 * C::B_BYTES);
+        for (int tap = 0; tap < 9; ++tap)
+          tma_load_2d(sB + ((tap % 3) * 3 + (2 - tap / 3)) * C::B_BYTES, &tb, &b_full[0], tap * p.kcp, 0);
+      } else if (WRES) {  // all weight tiles once (single N tile: the planner guarantees n_tiles == 1)
         mbar_expect_tx(&b_full[0], groups * nb * C::B_BYTES);
         for (int g = 0; g < groups; ++g)
           for (int j = 0; j < nb; ++j) {
@@ -1029,6 +1052,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // instruction), and at ~20 instructions per MMA it could not keep the N=32..128 MMAs
         // (45-65 clk each) fed -- the tile ran at half the tensor rate. Streamed weights (not
         // WRES) arrive one tap tile per ring slot.
+        if (dys) {
+          const int sa = ia % C::A_STAGES;
+          mbar_wait(&a_full[sa], (ia / C::A_STAGES) & 1);
+          ROLE_TRACE(0, tix, 2);
+          tc_fence_after();
+          const uint32_t a_lo = a_lo0 + (uint32_t)sa * (C::A_MAX >> 4);
+#pragma unroll
+          for (int h = 0; h < RT + 2; ++h) {
+            const int r_lo = h > 2 ? h - 2 : 0, r_hi = h < RT - 1 ? h : RT - 1;
+            const uint32_t id = idesc_bf16(128, (r_hi - r_lo + 1) * BN);
+            const int blk0 = 2 - (h - r_lo);  // block of row r_lo's kernel row dy = h - r_lo
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+              const uint32_t at = a_lo + (uint32_t)(h * P + dx) * (C::RB / 16);
+              const uint32_t bt = b_lo0 + (uint32_t)((dx * 3 + blk0) * (C::B_BYTES >> 4));
+#pragma unroll
+              for (int k = 0; k < KC / 2; ++k) {
+                const uint64_t ad = ((uint64_t)a_hi << 32) | (at + (uint32_t)k * kstep);
+                const uint64_t bd = ((uint64_t)b_hi << 32) | (bt + (uint32_t)(k * 2));
+                umma_f16(d + r_lo * BN, ad, bd, id, 1u);
+              }
+            }
+          }
+          umma_commit(&a_empty[sa]);
+          ++ia;
+          ROLE_TRACE(0, tix, 3);
+          umma_commit(&tfull[acc]);
+          continue;
+        }
         for (int g = 0; g < groups; ++g, ++ia) {
           const int sa = ia % C::A_STAGES;
           mbar_wait(&a_full[sa], (ia / C::A_STAGES) & 1);
@@ -1111,6 +1163,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         } else {
           tmem_ld32(tmem + (acc * RT + rt) * BN + ((uint32_t)(q * 32) << 16) + c0, v);
           tmem_ld_wait();
+          if (dys) {
+            tmem_zero32(tmem + (acc * RT + rt) * BN + ((uint32_t)(q * 32) << 16) + c0);
+            tmem_st_wait();
+          }
         }
         if (k + split >= RT * (BN / 32)) {  // last TMEM read of the tile by this warp
           tc_fence_before();

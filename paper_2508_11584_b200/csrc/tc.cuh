@@ -211,6 +211,14 @@ VPE_DEV void tmem_st32(uint32_t taddr, const float (&v)[32]) {
       "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+// zero 32 columns of this warp's 32 TMEM lanes (x8 stores of one zero register)
+VPE_DEV void tmem_zero32(uint32_t taddr) {
+  const uint32_t z = 0;
+#pragma unroll
+  for (int c = 0; c < 32; c += 8)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr + c), "r"(z)
+                 : "memory");
+}
 VPE_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 
