@@ -722,13 +722,15 @@ int launch_attention(const AttnPlan& a, cudaStream_t s) {
            : poly == 4 ? attention_tc_kernel<0x2525>
            : poly == 5 ? attention_tc_kernel<0x5555>
                        : attention_tc_kernel<0x1111>;
-  // Never PDL-launched: with the attention kernel in the programmatic chain the engine's outputs
-  // vary bitwise run to run (tools/pdl_determinism.py, VPE_PDL_MASK bisection: every mask that
-  // includes the attention kernel, even with griddepcontrol.wait moved to its first instruction;
-  // an isolated QKV GEMM -> attention chain, eager or graph-captured, stays deterministic, so the
-  // root cause is not pinned). It costs the one launch gap per layer.
+  // In the programmatic chain like every backbone kernel (VPE_ATT_PDL=0 takes it out). Round 1
+  // kept it out: with it in, engine outputs varied bitwise run to run. The likely cause was this
+  // kernel's own tail-tile race (inactive softmax warps ran ahead on p_full before PV(j-1) had
+  // consumed P; since fixed in the softmax loop), which PDL's tighter overlap exposed more often:
+  // after that fix tools/pdl_determinism.py finds 0 of 300 PDL replays differing bitwise
+  // (batch 1; 0 of 100 at batch 4).
+  static const int att_pdl = getenv("VPE_ATT_PDL") ? atoi(getenv("VPE_ATT_PDL")) : 1;
   const int saved_scope = pdl_scope();
-  pdl_scope() = 0;
+  if (!att_pdl) pdl_scope() = 0;
   struct Restore {
     int v;
     ~Restore() { pdl_scope() = v; }

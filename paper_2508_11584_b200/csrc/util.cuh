@@ -36,12 +36,11 @@ struct OncePerDevice {
   }
 };
 // Programmatic dependent launch: a process-wide switch set per engine before it captures its
-// graphs (vpe_set_pdl; VPE_PDL=0/1 overrides). Measured: latency mode (batch 1) backbone 0.752 ->
-// 0.695 ms and head p50 -8..-9%; throughput mode with concurrent head streams 3.51 -> 3.57 ms
-// per step (early-scheduled dependents hold SM slots the head kernels could use). Engines leave
-// it OFF by default: with it on, engine outputs varied bitwise in ~10% of replays even with the
-// attention kernel (the most frequent offender) kept out of the chain (tools/pdl_determinism.py,
-// VPE_PDL_MASK bisection) -- root cause not pinned, so it stays an opt-in latency experiment.
+// graphs (vpe_set_pdl; VPE_PDL=0/1 overrides). Engines turn it on for small batches (latency
+// mode: batch-1 p50 depth 1.01 -> 0.94 ms, seg 0.73 -> 0.66, det 0.83 -> 0.77) and leave it off
+// for throughput batches (C2 batch 16: 5285 -> 5194 fps with it, early-scheduled dependents hold
+// SM slots the concurrent head kernels could use). Bit-identical over 300 replays
+// (tools/pdl_determinism.py) since the attention kernel's tail-tile race was fixed.
 inline int& pdl_flag() {
   static int on = 0;
   return on;

@@ -179,10 +179,10 @@ class VPEngine:
         ``shared`` exports the ring for out-of-process consumers (channels.open_channel)."""
         torch.cuda.set_device(device)
         self.device = torch.device(f"cuda:{device}")
-        # programmatic dependent launch (opt-in): shortens latency-bound small batches (backbone
-        # 0.752 -> 0.695 ms at batch 1) but with it the outputs were observed to vary bitwise in
-        # ~10% of replays (tools/pdl_determinism.py; csrc/util.cuh), so it is off by default
-        self.pdl = False if pdl is None else bool(pdl)
+        # programmatic dependent launch: on by default for small batches (latency mode: batch-1
+        # p50 depth 1.01 -> 0.94 ms), off for throughput batches where it measured slower
+        # (csrc/util.cuh); outputs bit-identical either way (tools/pdl_determinism.py)
+        self.pdl = (batch <= 4) if pdl is None else bool(pdl)
         check(lib.vpe_set_pdl(int(self.pdl)), "vpe_set_pdl")
         self.cfg = model_config(model)
         self.model, self.resolution, self.batch = model, resolution, batch

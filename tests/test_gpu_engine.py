@@ -54,24 +54,49 @@ def test_graph_replay_deterministic(eng):
             assert torch.equal(a[n][k], b[n][k]), (n, k)
 
 
-def test_latency_mode_deterministic():
-    """Default (PDL off) latency-mode engine: every replay bit-identical (with programmatic
-    dependent launch on, outputs varied run to run -- tools/pdl_determinism.py)."""
+@pytest.mark.parametrize("batch,pdl", [(1, True), (2, True), (2, False)])
+def test_latency_mode_deterministic(batch, pdl):
+    """Latency-mode engine (programmatic dependent launch on by default at small batch, and off):
+    every replay bit-identical -- all head outputs and the ring taps (tools/pdl_determinism.py
+    runs the same check over 300 replays)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA")
     from paper_2508_11584_b200.engine import VPEngine
-    e = VPEngine("vits14", 448, 2)
+    e = VPEngine("vits14", 448, batch, pdl=pdl)
+    assert e.pdl == pdl
     try:
-        frames = make_frames(2, 448, 9)
-        ref = e.run(frames)
-        ref = {n: {k: v.clone() for k, v in o.items()} for n, o in ref.items()}
-        for _ in range(6):
+        e.channel.register_consumer(99)
+        frames = make_frames(batch, 448, 9)
+
+        def grab():
             o = e.run(frames)
-            for n in ref:
-                for k in ref[n]:
-                    assert torch.equal(o[n][k], ref[n][k]), (n, k)
+            out = {f"{n}.{k}": v.clone() for n, d in o.items() for k, v in d.items() if torch.is_tensor(v)}
+            lease = e.channel.acquire_latest(99)
+            for lab, v in e.channel.view(lease).items():
+                out[f"tap.{lab}"] = v.clone()
+            e.channel.commit(lease)
+            return out
+
+        ref = grab()
+        for _ in range(30):
+            o = grab()
+            for k in ref:
+                assert torch.equal(o[k], ref[k]), k
     finally:
         e.close()
+
+
+def test_engine_pdl_default():
+    """PDL defaults: on for latency batches, off for throughput batches."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    from paper_2508_11584_b200.engine import VPEngine
+    for b, want in ((1, True), (16, False)):
+        e = VPEngine("vits14", 224, b)
+        try:
+            assert e.pdl is want
+        finally:
+            e.close()
 
 
 def test_ring_counters_and_rates(eng):
