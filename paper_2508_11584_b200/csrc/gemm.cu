@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // 9 x RT x KC/2, the A operand read once per halo row instead of once per (row, dy). Same
   // per-row accumulation order as the tap loop (dy-major, dx, k). Every MMA accumulates, so the
   // epilogue zeroes each accumulator chunk after reading it (and all of TMEM starts at zero).
-  const bool dys = RT >= 2 && WRES && p.parts == 1 && groups == 1;
+  const bool dys = RT >= 2 && WRES && p.parts == 1 && groups == 1 && p.bh == RT;
   if (dys && warp >= 2) {
     const int e = warp - 2;
     for (int c = e >> 2; c < C::TMEM_COLS / 32; c += EPI_SPLIT)
@@ -1026,13 +1026,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // SW128 starts that are not 1024-aligned (any halo pixel) need no descriptor "base offset":
       // the swizzle is a function of the absolute smem address, which TMA and UMMA share
       // (measured: base offset = (addr >> 7) & 7 breaks every shifted tap)
+      const int rsub = p.bh / RT;  // output rows per 128-position sub-tile
       uint32_t toff[9 * RT];
       {
 #pragma unroll
         for (int tap = 0; tap < 9; ++tap)
 #pragma unroll
           for (int rt = 0; rt < RT; ++rt) {
-            const uint32_t px = (uint32_t)((rt + tap / 3) * P + tap % 3);  // halo pixel of the tap
+            const uint32_t px = (uint32_t)((rt * rsub + tap / 3) * P + tap % 3);  // halo pixel of the tap
             toff[tap * RT + rt] = C::SW ? px * (C::RB / 16) : px;
           }
       }
@@ -1774,10 +1775,20 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
     bw = W;
     P = W + 2;
     rows = 128 / P;
+    // streamed weights (too large to stay resident, e.g. the det head's 384 -> 384 hi+lo conv):
+    // two multi-row sub-tiles share each weight tile, halving the L2 -> SMEM weight traffic that
+    // bounds those convs (measured 7.3 TB/s of weight re-reads at 32 x 32)
+    const bool streamed = (size_t)parts * 9 * Cp * bn * 2 > (size_t)WRES_BYTES || (N + bn - 1) / bn > 1;
+    if (kc == 8 && bn == 128 && streamed && !getenv("VPE_HALO_NO_RT2")) {
+      const int rb2 = rows + 129 / P + 3;
+      if (rb2 * P <= 130 * 4) rt = 2;
+    }
   }
   static const double min_fill = getenv("VPE_HALO_FILL") ? atof(getenv("VPE_HALO_FILL")) : 0.7;
-  if (rows < 1 || (double)(rows * bw) / (128.0 * rt) < min_fill) return VPE_E_SHAPE;
-  const int rows_box = rt > 1 ? rt + 2 : 129 / P + 3;
+  const int rows_sub = W >= 128 ? 1 : rows;  // output rows per 128-position sub-tile
+  if (rows < 1 || (double)(rows_sub * bw) / 128.0 < min_fill) return VPE_E_SHAPE;
+  if (W < 128) rows = rows_sub * rt;  // output rows per tile
+  const int rows_box = W >= 128 ? (rt > 1 ? rt + 2 : 129 / P + 3) : (rt - 1) * rows_sub + 129 / P + 3;
   if (P > 256 || rows_box > 256) return VPE_E_SHAPE;
   if ((pitch_px * 2) % 16 || (pitch_row * 2) % 16 || (pitch_img * 2) % 16 || reinterpret_cast<uintptr_t>(X) % 16)
     return VPE_E_SHAPE;
@@ -1819,7 +1830,7 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   if (bn == BN_ && kc == KC_ && rt == RT_)                                           \
     g->smem = g->halo_wres ? HaloCfg<BN_, KC_, RT_, true>::SMEM : HaloCfg<BN_, KC_, RT_>::SMEM;
   VPE_HS(32, 4, 1) VPE_HS(64, 4, 1) VPE_HS(128, 4, 1) VPE_HS(32, 8, 1) VPE_HS(64, 8, 1) VPE_HS(128, 8, 1)
-  VPE_HS(32, 4, 4) VPE_HS(32, 8, 2) VPE_HS(64, 8, 2)
+  VPE_HS(32, 4, 4) VPE_HS(32, 8, 2) VPE_HS(64, 8, 2) VPE_HS(128, 8, 2)
 #undef VPE_HS
   return VPE_OK;
 }
@@ -2056,7 +2067,7 @@ int launch_gemm(const GemmPlan& g, cudaStream_t s) {
   if (g.bn == BN_ && g.halo_kc == KC_ && g.halo_rt == RT_)                            \
     return g.halo_wres ? launch_halo_t<BN_, KC_, RT_, true>(g, s) : launch_halo_t<BN_, KC_, RT_>(g, s);
     VPE_LH(32, 4, 1) VPE_LH(64, 4, 1) VPE_LH(128, 4, 1) VPE_LH(32, 8, 1) VPE_LH(64, 8, 1) VPE_LH(128, 8, 1)
-    VPE_LH(32, 4, 4) VPE_LH(32, 8, 2) VPE_LH(64, 8, 2)
+    VPE_LH(32, 4, 4) VPE_LH(32, 8, 2) VPE_LH(64, 8, 2) VPE_LH(128, 8, 2)
 #undef VPE_LH
     return VPE_E_SHAPE;
   }
