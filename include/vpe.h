@@ -330,8 +330,9 @@ int vpe_event_destroy(void* ev);
 int vpe_stream_wait_event(void* stream, void* ev);
 int vpe_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
 int64_t vpe_kernel_launches(void);
-/* programmatic dependent launch for kernels enqueued (or graph-captured) from now on: on for
- * latency-bound small batches, off for throughput (see csrc/util.cuh); VPE_PDL env overrides */
+/* programmatic dependent launch for the backbone kernels enqueued (or graph-captured) from now
+ * on: 0 off, 1 dependents released at kernel start, 2 released after each persistent kernel's last
+ * TMA load (see csrc/util.cuh); VPE_PDL / VPE_PDL_LATE env override */
 int vpe_set_pdl(int32_t on);    /* kernels enqueued by libvpe since load (graph replays count per node) */
 const char* vpe_status_str(int status);
 /* diagnostics: timeline of attention CTA 0 when the process runs with VPE_ATT_TRACE=1

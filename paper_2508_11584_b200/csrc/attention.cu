@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   pdl_wait();
-  pdl_trigger();
+  const bool pdl_late = (trace >> 8) & 1;  // signal dependents after the last K/V load
+  if (!pdl_late) pdl_trigger();
 
   // Units are ordered pair-major, so a unit without a B tile (T <= q0 + 128) is followed only by
   // such units: the slot-B barriers are simply left alone from then on.
@@ -303,6 +304,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
           tma_load_2d(sV + vs * TILE, &tqkv, &v_full[vs], 2 * D + w.h * 64, row0 + j * 128);
         }
       }
+      if (pdl_late) pdl_trigger();
     }
   } else if (warp == 1 || warp == 2) {
     // One MMA issuer warp per Q slot, so neither slot's PV/S issue queues behind the other's.
@@ -418,7 +420,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 1)
     int tn = 0;
     const bool tr = (quad == 0 && lane == 0 && hh == 0);
     const int tbase = 2048 + 1024 * x;
-    const int dbg = trace >> 1;  // diagnostics (VPE_ATT_DBG): 2 = no exp ping-pong
+    const int dbg = (trace >> 1) & 0x7f;  // diagnostics (VPE_ATT_DBG): 2 = no exp ping-pong
     const bool pp = !(dbg & 2);
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
     for (int ui = u_lo; ui < u_hi; ++ui) {
@@ -736,7 +738,7 @@ int launch_attention(const AttnPlan& a, cudaStream_t s) {
     ~Restore() { pdl_scope() = v; }
   } restore{saved_scope};
   return launch_k(k, dim3(a.grid), dim3(ATT_THREADS), SMEM_ATT, s, a.tqkv, a.out, a.B, a.T, a.D, a.heads, scale_log2,
-                  g_att_trace_on | (att_dbg() << 1), a.sched, a.single) == cudaSuccess
+                  g_att_trace_on | (att_dbg() << 1) | (pdl_late() << 8), a.sched, a.single) == cudaSuccess
              ? VPE_OK
              : VPE_E_CUDA;
 }

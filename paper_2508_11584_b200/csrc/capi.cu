@@ -159,7 +159,8 @@ int vpe_op_conv_up(const void* x, int32_t B, int32_t Hs, int32_t Ws, int32_t Cp,
 }
 
 int vpe_set_pdl(int32_t on) {
-  pdl_flag() = on ? 1 : 0;
+  if (on < 0 || on > 2) return VPE_E_VALUE;
+  pdl_flag() = on;
   return VPE_OK;
 }
 

@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   pdl_wait();
-  pdl_trigger();
+  if (!p.pdl_late) pdl_trigger();
   const int ntiles = p.m_tiles * p.n_tiles;
 
   if (warp == 0) {
@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tma_load_2d(sB + s * C::B_BYTES, &tb, &full[s], kb * BK, n0);
         }
       }
+      if (p.pdl_late) pdl_trigger();  // every load issued: the dependent grid may come in
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(RL_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
   pdl_wait();
-  pdl_trigger();
+  if (!p.pdl_late) pdl_trigger();
   const int m_tiles = p.m_tiles, kblocks = p.kblocks;
 
   if (warp == 0) {
@@ -686,6 +687,7 @@ __global__ void __launch_bounds__(RL_THREADS, 1)
           }
         }
       }
+      if (p.pdl_late) pdl_trigger();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -1977,6 +1979,7 @@ static int launch_t(const GemmPlan& g, cudaStream_t s) {
   }
   GemmParams p = g.p;
   p.trace = g_gemm_trace_on;
+  p.pdl_late = pdl_late();
   PdlKind pk(1);
   return launch_k(k, g.grid, dim3(GEMM_THREADS), GemmCfg<BN, BK>::SMEM, s, g.ta, g.tb, g.tout, p) == cudaSuccess
              ? VPE_OK
@@ -2038,6 +2041,7 @@ int launch_gemm_resid_ln(const GemmPlan& g0, __nv_bfloat16* xln, __nv_bfloat16* 
     g.p.ep.out = xln;
   }
   if (!g.p.ep.out) g.p.ln.w = nullptr;  // no LayerNorm output wanted (tap only)
+  g.p.pdl_late = pdl_late();
   CUtensorMap ttap;
   memset(&ttap, 0, sizeof(ttap));
   g.p.ln.tap = tap;

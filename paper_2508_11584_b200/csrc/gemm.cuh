@@ -72,6 +72,7 @@ struct GemmParams {
   // upsample-fused conv (conv_up_kernel): source map Hs x Ws, align_corners scales, source box
   int up_hs = 0, up_ws = 0, up_rows = 0, up_cols = 0, up_stages = 0, up_src_bytes = 0, up_box_bytes = 0;
   float up_sh = 0.f, up_sw = 0.f;
+  int pdl_late = 0;              // 1: signal programmatic dependents after the last TMA load, not at start
   int trace = 0;                 // diagnostics: record the MMA timeline of CTA 0
   int dbg = 0;                   // diagnostics (halo conv, VPE_HALO_DBG): 1 no stores, 2 no A reloads, 4 no MMA
   EpiParams ep;

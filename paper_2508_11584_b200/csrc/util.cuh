@@ -35,12 +35,14 @@ struct OncePerDevice {
     return !(done.fetch_or(bit, std::memory_order_acq_rel) & bit);
   }
 };
-// Programmatic dependent launch: a process-wide switch set per engine before it captures its
-// graphs (vpe_set_pdl; VPE_PDL=0/1 overrides). Engines turn it on for small batches (latency
-// mode: batch-1 p50 depth 1.01 -> 0.94 ms, seg 0.73 -> 0.66, det 0.83 -> 0.77) and leave it off
-// for throughput batches (C2 batch 16: 5285 -> 5194 fps with it, early-scheduled dependents hold
-// SM slots the concurrent head kernels could use). Bit-identical over 300 replays
-// (tools/pdl_determinism.py) since the attention kernel's tail-tile race was fixed.
+// Programmatic dependent launch: a process-wide mode set per engine before it captures its
+// graphs (vpe_set_pdl: 0 off, 1 early release, 2 late release; VPE_PDL=0/1 overrides on/off).
+// Early release (dependents launched as soon as each kernel passed its own griddepcontrol.wait)
+// helped batch 1 but cost throughput batches (C2 batch 16: 5285 -> 5194 fps: dependents parked on
+// SMs for a whole kernel, SMs the concurrent head kernels could have used). Late release (see
+// pdl_late) wins both: batch-1 p50 depth 1.01 -> 0.94 ms, batch 16 5272 -> 5380 fps. Outputs are
+// bit-identical over 300 replays (tools/pdl_determinism.py) since the attention kernel's tail-tile
+// race was fixed.
 inline int& pdl_flag() {
   static int on = 0;
   return on;
@@ -61,7 +63,19 @@ inline bool pdl_enabled() {
     env = e ? (e[0] == '1' ? 1 : 0) : -1;
   }
   if (!pdl_scope()) return false;
-  return env >= 0 ? env == 1 : pdl_flag() == 1;
+  return env >= 0 ? env == 1 : pdl_flag() != 0;
+}
+// Trigger placement: early (each kernel lets its dependents launch right after its own
+// griddepcontrol.wait) or late (the persistent GEMM / attention kernels signal after their last
+// TMA load, so the dependent grid occupies SMs only for the final tiles' drain). vpe_set_pdl(2)
+// selects late, vpe_set_pdl(1) early; VPE_PDL_LATE=0/1 overrides.
+inline int pdl_late() {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("VPE_PDL_LATE");
+    env = e ? atoi(e) : -1;
+  }
+  return env >= 0 ? env : (pdl_flag() == 2 ? 1 : 0);
 }
 // diagnostics: VPE_PDL_MASK limits PDL to kernel kinds (1 GEMM, 2 attention, 4 LayerNorm,
 // 8 halo conv, 16 im2col); a guard drops the scope for kinds outside the mask

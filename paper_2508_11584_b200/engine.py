@@ -179,11 +179,11 @@ class VPEngine:
         ``shared`` exports the ring for out-of-process consumers (channels.open_channel)."""
         torch.cuda.set_device(device)
         self.device = torch.device(f"cuda:{device}")
-        # programmatic dependent launch: on by default for small batches (latency mode: batch-1
-        # p50 depth 1.01 -> 0.94 ms), off for throughput batches where it measured slower
-        # (csrc/util.cuh); outputs bit-identical either way (tools/pdl_determinism.py)
-        self.pdl = (batch <= 4) if pdl is None else bool(pdl)
-        check(lib.vpe_set_pdl(int(self.pdl)), "vpe_set_pdl")
+        # programmatic dependent launch with late release (each persistent backbone kernel lets
+        # its dependent launch after its last TMA load): batch-1 p50 depth 1.01 -> 0.94 ms, C2
+        # batch 16 5272 -> 5380 fps (csrc/util.cuh); outputs bit-identical (tools/pdl_determinism.py)
+        self.pdl = True if pdl is None else bool(pdl)
+        check(lib.vpe_set_pdl(2 if self.pdl else 0), "vpe_set_pdl")
         self.cfg = model_config(model)
         self.model, self.resolution, self.batch = model, resolution, batch
         head_specs = [(h, BUILTIN_HEADS[h]) if isinstance(h, str) else (str(h[0]), str(h[1])) for h in heads]

@@ -54,7 +54,7 @@ def test_graph_replay_deterministic(eng):
             assert torch.equal(a[n][k], b[n][k]), (n, k)
 
 
-@pytest.mark.parametrize("batch,pdl", [(1, True), (2, True), (2, False)])
+@pytest.mark.parametrize("batch,pdl", [(1, True), (2, True), (16, True), (2, False)])
 def test_latency_mode_deterministic(batch, pdl):
     """Latency-mode engine (programmatic dependent launch on by default at small batch, and off):
     every replay bit-identical -- all head outputs and the ring taps (tools/pdl_determinism.py
@@ -87,12 +87,12 @@ def test_latency_mode_deterministic(batch, pdl):
 
 
 def test_engine_pdl_default():
-    """PDL defaults: on for latency batches, off for throughput batches."""
+    """PDL (late release) is the default at every batch size; pdl=False turns it off."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA")
     from paper_2508_11584_b200.engine import VPEngine
-    for b, want in ((1, True), (16, False)):
-        e = VPEngine("vits14", 224, b)
+    for b, kw, want in ((1, {}, True), (16, {}, True), (1, {"pdl": False}, False)):
+        e = VPEngine("vits14", 224, b, **kw)
         try:
             assert e.pdl is want
         finally:
