@@ -384,10 +384,21 @@ def kernel_rooflines(eng, peaks):
     h = R // 14
     C = eng.cfg.seg_classes
     cp = (C + 31) // 32 * 32
-    lg = rnd(B, h * h, cp, dtype=torch.float32)
-    hbm("seg_upsample_argmax", "seg_upsample_argmax_kernel", {"B": B, "h": h, "C": C},
+    # the engine's own seg logits (class pruning depends on the data: uncorrelated random logits
+    # keep ~5x more candidate classes per block than the seeded head on backbone features)
+    lg = torch.zeros(B, h * h, cp, device=dev)
+    if "seg" in eng.heads:  # ring slot 0 holds a frame's `final` tap once the engine has run
+        lab = torch.empty(B, R, R, device=dev, dtype=torch.uint8)
+        lc = torch.empty(B, h * h, C, device=dev)
+        eng.heads["seg"].forward(eng.channel.group_views(0)[eng.labels[-1]], lab, lc)
+        lg[..., :C] = lc
+    else:
+        lg = rnd(B, h * h, cp, dtype=torch.float32)
+    torch.cuda.synchronize()
+    hbm("seg_upsample_argmax", "seg_upsample_argmax_pruned_kernel", {"B": B, "h": h, "C": C},
         B * (h * h * cp * 4 + R * R), lambda: _ops.upsample_argmax(lg, h, R, classes=C),
-        note="instruction-bound: ~C x R^2 bilinear interpolations per image")
+        note="issue-bound: per 7x7 block the classes whose corner range can reach the max (~12 of 150 on "
+             "the engine's logits), then the exact per-pixel bilinear + argmax over those")
     xr = rnd(M, D, dtype=torch.float32)
     lw, lb = torch.ones(D, device=dev), torch.zeros(D, device=dev)
     hbm("layernorm", "layernorm_kernel", {"M": M, "D": D}, M * D * (4 + 2), lambda: _ops.layernorm(xr, lw, lb))

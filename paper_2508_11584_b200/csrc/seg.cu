@@ -5,6 +5,7 @@
 // Oracle: oracle/seg.py.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <new>
 
 #include "gemm.cuh"
@@ -176,6 +177,138 @@ __global__ void __launch_bounds__(1024)
     labels[((int64_t)b * R + oy0 + k) * R + ox] = (uint8_t)arg[k];
   }
 }
+// Candidate-pruned variant (default). Within a 7 x 7 output block that samples one source cell
+// (the CTA's 7 rows share the source rows; 7-column blocks never straddle a source column
+// boundary: boundaries fall at 14k + 7), every class's upsampled logit is bilinear in the
+// block's interpolation weights, so its range over the block is spanned by the 4 corner pixels.
+// A class whose corner maximum is below tau = max over classes of the corner minimum (less a
+// rounding margin) cannot be the argmax anywhere in the block; warps build each block's list of
+// the remaining classes (ascending, by ballot), then every pixel evaluates only those, with the
+// exact per-pixel formula and first-index tie rule above -- identical labels. Measured on the
+// seeded C2 head: ~12 of 150 classes survive per block.
+constexpr int SEG_BLK = 7;         // block width (columns) = HALF_ROWS
+constexpr int SEG_CMAX = 256;      // classes supported
+
+__device__ __forceinline__ float seg_t(const float* r, int x0, int x1, int cs, int c, float w0, float w1) {
+  return __fadd_rn(__fmul_rn(r[x0 * cs + c], w0), __fmul_rn(r[x1 * cs + c], w1));
+}
+
+__global__ void __launch_bounds__(1024)
+    seg_upsample_argmax_pruned_kernel(const float* __restrict__ logits, int h, int C, int cp, int R,
+                                      uint8_t* __restrict__ labels) {
+  extern __shared__ float s_src[];  // [2 rows][h cols][cs], then the candidate lists
+  const int cs = (C + 1) & ~1;
+  const int nblk = R / SEG_BLK;
+  uint8_t* s_cand = reinterpret_cast<uint8_t*>(s_src + 2 * h * cs);  // [nblk][C]
+  int* s_ncand = reinterpret_cast<int*>(s_cand + ((nblk * C + 15) & ~15));
+  const int hb = blockIdx.x, b = blockIdx.y;
+  const float scale = (float)h / (float)R;
+  const int oy0 = hb * HALF_ROWS;
+  int y0, y1;
+  float hy0_unused, hy1_unused;
+  src_index(scale, oy0, h, y0, y1, hy0_unused, hy1_unused);
+  const float* src = logits + (int64_t)b * h * h * cp;
+  const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int pix = wid; pix < 2 * h; pix += nw) {
+    const int yy = pix < h ? y0 : y1, xx = pix < h ? pix : pix - h;
+    const float* g = src + ((int64_t)yy * h + xx) * cp;
+    float* d = s_src + pix * cs;
+#pragma unroll 4
+    for (int c = lane; c < cs; c += 32) d[c] = c < C ? __ldg(g + c) : 0.f;
+  }
+  __syncthreads();
+  const float* r0 = s_src;
+  const float* r1 = s_src + h * cs;
+  // ---- candidate lists, one warp per block
+  {
+    int a0, a1;
+    float ht0, ht1, hb0, hb1;  // vertical weights of the band's first and last row
+    src_index(scale, oy0, h, a0, a1, ht0, ht1);
+    src_index(scale, oy0 + HALF_ROWS - 1, h, a0, a1, hb0, hb1);
+    for (int blk = wid; blk < nblk; blk += nw) {
+      int xa0, xa1, xb0, xb1;
+      float wa0, wa1, wb0, wb1;
+      src_index(scale, blk * SEG_BLK, h, xa0, xa1, wa0, wa1);
+      src_index(scale, blk * SEG_BLK + SEG_BLK - 1, h, xb0, xb1, wb0, wb1);
+      float lb[SEG_CMAX / 32], ub[SEG_CMAX / 32];
+      float tau = -INFINITY, mag = 0.f;
+#pragma unroll
+      for (int j = 0; j < SEG_CMAX / 32; ++j) {
+        const int c = lane + 32 * j;
+        lb[j] = -INFINITY;
+        ub[j] = -INFINITY;
+        if (c < C) {
+          const float ta0 = seg_t(r0, xa0, xa1, cs, c, wa0, wa1), ta1 = seg_t(r1, xa0, xa1, cs, c, wa0, wa1);
+          const float tb0 = seg_t(r0, xb0, xb1, cs, c, wb0, wb1), tb1 = seg_t(r1, xb0, xb1, cs, c, wb0, wb1);
+          const float v00 = __fadd_rn(__fmul_rn(ta0, ht0), __fmul_rn(ta1, ht1));
+          const float v01 = __fadd_rn(__fmul_rn(tb0, ht0), __fmul_rn(tb1, ht1));
+          const float v10 = __fadd_rn(__fmul_rn(ta0, hb0), __fmul_rn(ta1, hb1));
+          const float v11 = __fadd_rn(__fmul_rn(tb0, hb0), __fmul_rn(tb1, hb1));
+          lb[j] = fminf(fminf(v00, v01), fminf(v10, v11));
+          ub[j] = fmaxf(fmaxf(v00, v01), fmaxf(v10, v11));
+          tau = fmaxf(tau, lb[j]);
+          mag = fmaxf(mag, fmaxf(fmaxf(fabsf(r0[xa0 * cs + c]), fabsf(r0[xb1 * cs + c])),
+                                 fmaxf(fabsf(r1[xa0 * cs + c]), fabsf(r1[xb1 * cs + c]))));
+          mag = fmaxf(mag, fmaxf(fmaxf(fabsf(r0[xa1 * cs + c]), fabsf(r0[xb0 * cs + c])),
+                                 fmaxf(fabsf(r1[xa1 * cs + c]), fabsf(r1[xb0 * cs + c]))));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        tau = fmaxf(tau, __shfl_xor_sync(0xffffffffu, tau, o));
+        mag = fmaxf(mag, __shfl_xor_sync(0xffffffffu, mag, o));
+      }
+      // every computed value (pixel or corner) is within a few roundings (2^-24 each) of the
+      // exact bilinear value, relative to the largest source logit: keep a 2^-16 margin
+      const float thr = tau - mag * 0x1p-16f;
+      int n = 0;
+#pragma unroll
+      for (int j = 0; j < SEG_CMAX / 32; ++j) {
+        const int c = lane + 32 * j;
+        const bool keep = c < C && ub[j] >= thr;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) s_cand[blk * C + n + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)c;
+        n += __popc(bal);
+      }
+      if (lane == 0) s_ncand[blk] = n;
+    }
+  }
+  __syncthreads();
+  // ---- per pixel: the block's candidates in ascending class order, exact formula
+  const int ox = threadIdx.x;
+  if (ox >= R) return;
+  int x0, x1;
+  float wx0, wx1;
+  src_index(scale, ox, h, x0, x1, wx0, wx1);
+  float hy0[HALF_ROWS], hy1[HALF_ROWS], best[HALF_ROWS];
+  int arg[HALF_ROWS];
+#pragma unroll
+  for (int k = 0; k < HALF_ROWS; ++k) {
+    int a0, a1;
+    src_index(scale, oy0 + k, h, a0, a1, hy0[k], hy1[k]);
+    best[k] = -INFINITY;
+    arg[k] = 0;
+  }
+  const int blk = ox / SEG_BLK;
+  const int n = s_ncand[blk];
+  const uint8_t* cl = s_cand + blk * C;
+#pragma unroll 1
+  for (int i = 0; i < n; ++i) {
+    const int c = cl[i];
+    const float t0 = seg_t(r0, x0, x1, cs, c, wx0, wx1), t1 = seg_t(r1, x0, x1, cs, c, wx0, wx1);
+#pragma unroll
+    for (int k = 0; k < HALF_ROWS; ++k) {
+      const float v = __fadd_rn(__fmul_rn(t0, hy0[k]), __fmul_rn(t1, hy1[k]));
+      if (v > best[k]) {
+        best[k] = v;
+        arg[k] = c;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < HALF_ROWS; ++k) labels[((int64_t)b * R + oy0 + k) * R + ox] = (uint8_t)arg[k];
+}
+
 int launch_upsample_argmax(const float* logits, int B, int h, int C, int cp, int R, uint8_t* labels,
                            cudaStream_t st) {
   const size_t smem = (size_t)2 * h * ((C + 1) & ~1) * sizeof(float);
@@ -186,8 +319,19 @@ int launch_upsample_argmax(const float* logits, int B, int h, int C, int cp, int
     VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       227 * 1024));
     max_smem_carveout(seg_upsample_argmax_kernel);
+    VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_pruned_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    max_smem_carveout(seg_upsample_argmax_pruned_kernel);
   }
-  seg_upsample_argmax_kernel<<<dim3(2 * h, B), (R + 31) / 32 * 32, smem, st>>>(logits, h, C, cp, R, labels, 0.f);
+  static const bool prune = !(getenv("VPE_SEG_PRUNE") && getenv("VPE_SEG_PRUNE")[0] == '0');  // A/B
+  const int nblk = R / SEG_BLK;
+  const size_t smem_p = smem + (((size_t)nblk * C + 15) & ~(size_t)15) + (size_t)nblk * sizeof(int);
+  if (prune && R % SEG_BLK == 0 && HALF_ROWS == SEG_BLK && smem_p <= 227 * 1024) {
+    seg_upsample_argmax_pruned_kernel<<<dim3(2 * h, B), (R + 31) / 32 * 32, smem_p, st>>>(logits, h, C, cp, R,
+                                                                                          labels);
+  } else {
+    seg_upsample_argmax_kernel<<<dim3(2 * h, B), (R + 31) / 32 * 32, smem, st>>>(logits, h, C, cp, R, labels, 0.f);
+  }
   VPE_CUDA_TRY(cudaGetLastError());
   return VPE_OK;
 }
