@@ -166,3 +166,53 @@ def test_upsample_argmax_exact(B, h, C, cp):
     ref = ref.to(torch.uint8)
     bad = (labels.cpu() != ref).sum().item()
     assert bad == 0, f"{bad} of {ref.numel()} labels differ"
+
+
+def _upsample_argmax_formula(lg: torch.Tensor, h: int, C: int, R: int) -> torch.Tensor:
+    """CPU fp32 restatement of the kernels' per-pixel arithmetic (oracle/seg.py's bilinear,
+    align_corners=False, in torch's channels-last rounding order: s = fma(scale, o + 0.5, -0.5),
+    value = (a*w0 + b*w1)*h0 + (c*w0 + d*w1)*h1, every op rounded to fp32) + first-index argmax."""
+    scale = torch.tensor(h, dtype=torch.float32) / torch.tensor(R, dtype=torch.float32)
+    o = torch.arange(R, dtype=torch.float64) + 0.5
+    src = (scale.double() * o - 0.5).float().clamp_min(0.0)  # one rounding: the fma
+    i0 = src.long()
+    i1 = torch.where(i0 < h - 1, i0 + 1, i0)
+    l1 = (src - i0.float()).clamp(0.0, 1.0)
+    l0 = 1.0 - l1
+    B = lg.shape[0]
+    x = lg[..., :C].reshape(B, h, h, C)
+    out = torch.empty(B, R, R, dtype=torch.uint8)
+    for oy in range(R):
+        r0, r1 = x[:, i0[oy]], x[:, i1[oy]]  # [B, h, C]
+        t0 = r0[:, i0] * l0[None, :, None] + r0[:, i1] * l1[None, :, None]  # [B, R, C]
+        t1 = r1[:, i0] * l0[None, :, None] + r1[:, i1] * l1[None, :, None]
+        v = t0 * l0[oy] + t1 * l1[oy]
+        out[:, oy] = v.argmax(-1).to(torch.uint8)
+    return out
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_upsample_argmax_smooth_near_ties(seed):
+    """Class pruning (seg_upsample_argmax_pruned_kernel) on spatially smooth logits -- few
+    candidate classes per 7x7 block -- with classes within a few ulps of each other (and exact
+    ties), so the pruning margin decides: labels must equal the same arithmetic evaluated over
+    every class on the CPU. (Against torch's own interpolate such near-ties are decided by its
+    rounding order, not this kernel's; the exact-tie cases above are order-independent.)"""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    from paper_2508_11584_b200 import _ops
+    B, h, C, cp = 2, 32, 150, 160
+    R = 14 * h
+    g = torch.Generator().manual_seed(100 + seed)
+    coarse = torch.randn(B, C, 5, 5, generator=g)
+    x = torch.nn.functional.interpolate(coarse, size=(h, h), mode="bicubic", align_corners=True)
+    x[:, 3] = x[:, 7] * (1 + 2 ** -23 * torch.randint(-4, 5, (B, h, h), generator=g).float())
+    x[:, 9] = x[:, 11]
+    x[:, 20] = x.max(1).values  # a class equal to the per-pixel maximum at every source pixel
+    lg = torch.zeros(B, h * h, cp)
+    lg[..., :C] = x.permute(0, 2, 3, 1).reshape(B, h * h, C)
+    labels = _ops.upsample_argmax(lg.cuda(), h, R, classes=C)
+    torch.cuda.synchronize()
+    ref = _upsample_argmax_formula(lg, h, C, R)
+    bad = (labels.cpu() != ref).sum().item()
+    assert bad == 0, f"{bad} of {ref.numel()} labels differ"
