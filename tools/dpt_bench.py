@@ -12,10 +12,12 @@ from paper_2508_11584_b200.weights import make_weights
 
 
 def main():
-    B, R = int(os.environ.get("VPE_BATCH", "16")), 448
+    B = int(os.environ.get("VPE_BATCH", "16"))
+    model = os.environ.get("VPE_MODEL", "vits14")
+    R = int(os.environ.get("VPE_RES", "448"))
     dev = torch.device("cuda:0")
-    cfg = model_config("vits14")
-    W = make_weights("vits14")
+    cfg = model_config(model)
+    W = make_weights(model)
     taps = [torch.randn(B, tokens(R), cfg.backbone.dim, device=dev).to(torch.bfloat16) for _ in range(4)]
     head = DepthHead(W, cfg, R, B, dev)
     depth = torch.empty(B, R, R, device=dev)
@@ -29,7 +31,7 @@ def main():
         head.forward(taps, depth)
     b.record()
     torch.cuda.synchronize()
-    print(f"dpt head B={B} R={R}: {a.elapsed_time(b) / reps * 1e3:.1f} us/forward")
+    print(f"dpt head {model} B={B} R={R}: {a.elapsed_time(b) / reps * 1e3:.1f} us/forward")
 
 
 if __name__ == "__main__":
