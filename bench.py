@@ -582,7 +582,7 @@ def run_ours(args):
     p50_latency = latency_mode(args, W, local) if rank == 0 else None
     if rank == 0:
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N = 1 figure
             try:
                 cpu = cpu_baseline(args, cfg, W, args.cpu_seconds)
             except Exception as exc:  # reported, never fatal to the GPU number
