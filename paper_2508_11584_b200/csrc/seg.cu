@@ -381,8 +381,13 @@ extern "C" int vpe_seg_forward(vpe_seg* s, const void* final_tap, uint8_t* label
     ep.out = s->logits;
     ep.ldo = s->cpitch;
     const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(final_tap) + D;  // skip cls row
+    // one N tile covering all classes when there are enough pixel tiles to fill the GPU (the
+    // tap is then read once, not once per 32-class tile); narrow tiles for small batches
+    static const int bn_env = getenv("VPE_SEG_BN") ? atoi(getenv("VPE_SEG_BN")) : 0;  // A/B
+    const int m_tiles = (B * h * h + 127) / 128;
+    const int bn = bn_env ? bn_env : ((C <= 192 && m_tiles >= 64) ? (C <= 128 ? 128 : 192) : 32);
     VPE_TRY(plan_gemm_conv(&s->g, x, B, h, h, D, D, (int64_t)h * D, (int64_t)T * D, 1, 64,
-                           static_cast<const __nv_bfloat16*>(s->w.w_split), C, 2 * D, 2 * D, ep, 32));
+                           static_cast<const __nv_bfloat16*>(s->w.w_split), C, 2 * D, 2 * D, ep, bn));
     s->bound = final_tap;
   }
   VPE_TRY(launch_gemm(s->g, st));
