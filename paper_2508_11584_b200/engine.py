@@ -4,8 +4,8 @@ This is the B200 re-design of the reference's foundation loop / head loops (SPEC
 its control module and of the paper's multi-process, CUDA-IPC/MPS deployment
 (PAPER.md:95-121):
 
-* one process per GPU; the backbone runs on a producer stream, each head on its own
-  higher-priority stream (replaces MPS time-slicing between processes);
+* one process per GPU; the backbone runs on a producer stream, each head on its own stream
+  (replaces MPS time-slicing between processes; equal priorities by default, VPE_PRIO);
 * the backbone writes its four tap features straight into a LATEST ring slot
   (``channels.create_channel`` over ``vpe_ring``) — the "middle buffer" (PAPER.md:84);
 * each admitted head leases the newest slot, its stream waits on the slot's ready event, its
@@ -35,6 +35,7 @@ from __future__ import annotations
 
 import collections
 import ctypes as C
+import os
 import json
 import logging
 import threading
@@ -206,8 +207,12 @@ class VPEngine:
         self.channel, self.handle = create_channel("features", ChannelMode.LATEST, self.capacity, specs,
                                                    self.namespace, expected_consumers=len(self.heads),
                                                    device=device, shared=shared)
-        self.s_prod = _Stream(0)
-        self.s_head = {n: _Stream(-1) for n in self.heads}
+        # stream priorities (lower = higher), VPE_PRIO="prod,head". Equal by default: heads above
+        # the producer measured 1% lower C2 throughput (5454 vs 5514 fps) and the same latency-mode
+        # p50 (frames complete one at a time there)
+        prio = [int(v) for v in os.environ.get("VPE_PRIO", "0,0").split(",")]
+        self.s_prod = _Stream(prio[0])
+        self.s_head = {n: _Stream(prio[1]) for n in self.heads}
         now = time.monotonic_ns()
         rates = dict(rates or {})
         unknown = set(rates) - set(self.heads)
