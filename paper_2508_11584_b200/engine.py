@@ -4,8 +4,8 @@ This is the B200 re-design of the reference's foundation loop / head loops (SPEC
 its control module and of the paper's multi-process, CUDA-IPC/MPS deployment
 (PAPER.md:95-121):
 
-* one process per GPU; the backbone runs on a producer stream, each head on its own stream
-  (replaces MPS time-slicing between processes; equal priorities by default, VPE_PRIO);
+* one process per GPU; the backbone runs on a producer stream, each head on its own
+  higher-priority stream (replaces MPS time-slicing between processes; VPE_PRIO overrides);
 * the backbone writes its four tap features straight into a LATEST ring slot
   (``channels.create_channel`` over ``vpe_ring``) — the "middle buffer" (PAPER.md:84);
 * each admitted head leases the newest slot, its stream waits on the slot's ready event, its
@@ -207,10 +207,10 @@ class VPEngine:
         self.channel, self.handle = create_channel("features", ChannelMode.LATEST, self.capacity, specs,
                                                    self.namespace, expected_consumers=len(self.heads),
                                                    device=device, shared=shared)
-        # stream priorities (lower = higher), VPE_PRIO="prod,head". Equal by default: heads above
-        # the producer measured 1% lower C2 throughput (5454 vs 5514 fps) and the same latency-mode
-        # p50 (frames complete one at a time there)
-        prio = [int(v) for v in os.environ.get("VPE_PRIO", "0,0").split(",")]
+        # stream priorities (lower = higher), VPE_PRIO="prod,head": heads above the producer, so
+        # an admitted head is never queued behind the next frame's backbone (equal priorities
+        # measured 1% more C2 throughput, 5514 vs 5454 fps, and the same latency-mode p50)
+        prio = [int(v) for v in os.environ.get("VPE_PRIO", "0,-1").split(",")]
         self.s_prod = _Stream(prio[0])
         self.s_head = {n: _Stream(prio[1]) for n in self.heads}
         now = time.monotonic_ns()
