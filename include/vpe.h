@@ -329,11 +329,15 @@ int vpe_event_elapsed_ms(void* start, void* end, float* ms);
 int vpe_event_destroy(void* ev);
 int vpe_stream_wait_event(void* stream, void* ev);
 int vpe_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
-int64_t vpe_kernel_launches(void);
+int64_t vpe_kernel_launches(void); /* kernels enqueued by libvpe since load (graph replays count per node) */
 /* programmatic dependent launch for the backbone kernels enqueued (or graph-captured) from now
  * on: 0 off, 1 dependents released at kernel start, 2 released after each persistent kernel's last
  * TMA load (see csrc/util.cuh); VPE_PDL / VPE_PDL_LATE env override */
-int vpe_set_pdl(int32_t on);    /* kernels enqueued by libvpe since load (graph replays count per node) */
+int vpe_set_pdl(int32_t on);
+/* DPT reassemble / neck branches 0..2 on side streams (forked and joined with events, so
+ * graph capture records the DAG) for forwards enqueued from now on: -1 auto (on below batch 8,
+ * the default), 0 off, 1 on; VPE_DPT_BRANCHES env sets the initial mode */
+int vpe_set_dpt_branches(int32_t mode);
 const char* vpe_status_str(int status);
 /* diagnostics: timeline of attention CTA 0 when the process runs with VPE_ATT_TRACE=1
    ((code, clock64) pairs; see csrc/attention.cu) */

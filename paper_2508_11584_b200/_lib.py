@@ -148,6 +148,7 @@ _SIGS = {
     "vpe_op_linear": (i32, [vp, i32, i32, vp, i32, i32, vp, vp, vp, i32, i32, i32, vp]),
     "vpe_op_conv": (i32, [vp, i32, i32, i32, i32, i32, i32, vp, i32, vp, vp, vp, vp, vp, i32, i32, vp]),
     "vpe_set_pdl": (i32, [i32]),
+    "vpe_set_dpt_branches": (i32, [i32]),
     "vpe_debug_att_trace": (i32, [vp, i32]),
     "vpe_debug_gemm_trace": (i32, [vp, i32]),
     "vpe_op_attention": (i32, [vp, vp, i32, i32, i32, i32, vp]),

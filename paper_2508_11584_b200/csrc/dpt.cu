@@ -48,8 +48,54 @@ struct vpe_dpt {
   GemmPlan head2;  // epilogue pointers patched per call (depth outputs)
   bool fused_up = false;  // head1 / head2 read the un-resized maps (conv_up_kernel)
   bf16 *wpack1 = nullptr, *wpack2 = nullptr;  // their dy-stacked weights
+  // Reassemble + neck branches 0..2 run on side streams beside branch 3 and the first fusion
+  // stages (forked / joined with events, so graph capture records the same DAG).
+  cudaStream_t side[3] = {nullptr};
+  cudaEvent_t fork = nullptr, join[3] = {nullptr};
+  int side_prio = 1 << 30;
   int nkern = 0;
 };
+
+// Default: on for small batches, where each branch kernel leaves most SMs idle (batch-1 depth
+// p50 0.94 -> 0.88 ms); off at batch >= 8, where the branches already fill the GPU and the
+// engine overlaps the head with the next batch's backbone anyway (C2 unchanged within noise).
+// VPE_DPT_BRANCHES=0/1 forces it.
+static int& dpt_branch_mode() {
+  static int v = [] {
+    const char* e = getenv("VPE_DPT_BRANCHES");
+    return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+  }();
+  return v;
+}
+
+static bool dpt_branches_enabled(int B) {
+  const int v = dpt_branch_mode();
+  return v < 0 ? B < 8 : v != 0;
+}
+
+extern "C" int vpe_set_dpt_branches(int32_t mode) {
+  if (mode < -1 || mode > 1) return VPE_E_VALUE;
+  dpt_branch_mode() = mode;
+  return VPE_OK;
+}
+
+// Side streams carry the caller's priority (the engine runs heads above the producer).
+static int dpt_side_streams(vpe_dpt* d, cudaStream_t s) {
+  int prio = 0;
+  if (cudaStreamGetPriority(s, &prio) != cudaSuccess) return VPE_E_CUDA;
+  if (d->side[0] && prio == d->side_prio) return VPE_OK;
+  for (int i = 0; i < 3; ++i) {
+    if (d->side[i]) cudaStreamDestroy(d->side[i]);
+    d->side[i] = nullptr;
+  }
+  for (int i = 0; i < 3; ++i)
+    if (cudaStreamCreateWithPriority(&d->side[i], cudaStreamNonBlocking, prio) != cudaSuccess) return VPE_E_CUDA;
+  if (!d->fork && cudaEventCreateWithFlags(&d->fork, cudaEventDisableTiming) != cudaSuccess) return VPE_E_CUDA;
+  for (int i = 0; i < 3; ++i)
+    if (!d->join[i] && cudaEventCreateWithFlags(&d->join[i], cudaEventDisableTiming) != cudaSuccess) return VPE_E_CUDA;
+  d->side_prio = prio;
+  return VPE_OK;
+}
 
 static int conv_plan(GemmPlan* g, const bf16* x, int B, int S, int Cp, const void* w, int N, const EpiParams& ep) {
   const int kb = 9 * Cp;
@@ -96,6 +142,11 @@ extern "C" int vpe_dpt_destroy(vpe_dpt* d) {
   cudaFree(d->depth_pre_tmp);
   cudaFree(d->wpack1);
   cudaFree(d->wpack2);
+  for (int i = 0; i < 3; ++i) {
+    if (d->side[i]) cudaStreamDestroy(d->side[i]);
+    if (d->join[i]) cudaEventDestroy(d->join[i]);
+  }
+  if (d->fork) cudaEventDestroy(d->fork);
   delete d;
   return VPE_OK;
 }
@@ -252,19 +303,37 @@ extern "C" int vpe_dpt_forward(vpe_dpt* d, const void* const* taps, float* depth
   VPE_TRY(bind_taps(d, taps));
   const int B = d->B, F = d->F;
   int n = 0;
-  for (int i = 0; i < 4; ++i) {
-    VPE_TRY(launch_gemm(d->rs[i], s));
-    ++n;
-  }
-  VPE_TRY(launch_im2col_s2(d->r3a, B, d->h, d->h, d->Cp[3], d->r3col, s));
-  VPE_TRY(launch_gemm(d->rs3conv, s));
-  n += 2;
-  for (int i = 0; i < 4; ++i) {
-    VPE_TRY(launch_gemm(d->neck[i], s));
-    ++n;
+  const bool br = dpt_branches_enabled(B);
+  if (br) {
+    VPE_TRY(dpt_side_streams(d, s));
+    VPE_CUDA_TRY(cudaEventRecord(d->fork, s));
+    for (int i = 0; i < 3; ++i) {
+      VPE_CUDA_TRY(cudaStreamWaitEvent(d->side[i], d->fork, 0));
+      VPE_TRY(launch_gemm(d->rs[i], d->side[i]));
+      VPE_TRY(launch_gemm(d->neck[i], d->side[i]));
+      VPE_CUDA_TRY(cudaEventRecord(d->join[i], d->side[i]));
+    }
+    VPE_TRY(launch_gemm(d->rs[3], s));
+    VPE_TRY(launch_im2col_s2(d->r3a, B, d->h, d->h, d->Cp[3], d->r3col, s));
+    VPE_TRY(launch_gemm(d->rs3conv, s));
+    VPE_TRY(launch_gemm(d->neck[3], s));
+    n += 9;
+  } else {
+    for (int i = 0; i < 4; ++i) {
+      VPE_TRY(launch_gemm(d->rs[i], s));
+      ++n;
+    }
+    VPE_TRY(launch_im2col_s2(d->r3a, B, d->h, d->h, d->Cp[3], d->r3col, s));
+    VPE_TRY(launch_gemm(d->rs3conv, s));
+    n += 2;
+    for (int i = 0; i < 4; ++i) {
+      VPE_TRY(launch_gemm(d->neck[i], s));
+      ++n;
+    }
   }
   for (int k = 0; k < 4; ++k) {
     const int fi = 3 - k, S = d->S[fi];
+    if (br && k > 0) VPE_CUDA_TRY(cudaStreamWaitEvent(s, d->join[fi], 0));
     for (int j = (k > 0 ? 0 : 2); j < 4; ++j) {
       VPE_TRY(launch_gemm(d->rcu[k][j], s));
       ++n;

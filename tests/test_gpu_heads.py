@@ -79,6 +79,39 @@ def test_depth_fused_resize_bitexact(setup, monkeypatch):
         del head
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
 
+
+def test_depth_branches_bitexact(setup):
+    """Reassemble / neck branches on side streams (vpe_set_dpt_branches(1)), eager and captured in
+    a CUDA graph, write exactly the depth the single-stream order (0) writes."""
+    from paper_2508_11584_b200._lib import lib
+    from paper_2508_11584_b200.heads import DepthHead
+    s = setup
+    R, B, dev = s["R"], s["B"], s["dev"]
+    head = DepthHead(s["W"], s["cfg"], R, B, dev)
+    outs = []
+    try:
+        for mode in (0, 1):
+            assert lib.vpe_set_dpt_branches(mode) == 0
+            depth = torch.full((B, R, R), float("nan"), device=dev)
+            head.forward(s["taps"], depth)
+            torch.cuda.synchronize()
+            outs.append(depth.clone())
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side):
+            depth = torch.full((B, R, R), float("nan"), device=dev)
+            head.forward(s["taps"], depth)  # side streams at this stream's priority, before capture
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                head.forward(s["taps"], depth)
+        depth.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        outs.append(depth.clone())
+    finally:
+        lib.vpe_set_dpt_branches(-1)
+    assert lib.vpe_set_dpt_branches(2) != 0
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
 def test_seg_stagewise(setup):
     from paper_2508_11584_b200.heads import SegHead
     s = setup
