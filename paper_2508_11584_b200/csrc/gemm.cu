@@ -1479,15 +1479,20 @@ __global__ void __launch_bounds__(UP_THREADS, 1)
       if (tr) UP_TRACE(1020, tix, 22);
       const uint32_t src = smem_u32(sS + ss * SB);
       const uint32_t dst = smem_u32(sA + sa * C::A_BYTES);
+      // Each pass hands 2 jobs to each of the first `act` threads (the rest skip it) instead of
+      // 1-2 jobs to all of them: with KC = 4 (520 jobs, 320 threads) only 8 warps do the work.
 #pragma unroll 1
-      for (int jb = ((p.dbg & 1) ? C::JOBS : bt); jb < C::JOBS; jb += 2 * NB) {
+      for (int base = ((p.dbg & 1) ? C::JOBS : 0); base < C::JOBS; base += 2 * NB) {
+        const int rem = C::JOBS - base < 2 * NB ? C::JOBS - base : 2 * NB, act = (rem + 1) >> 1;
+        if (bt >= act) continue;
+        const int jb = base + bt;
         uint32_t s0[2], s1[2];
         uint64_t hx[2], lx[2], hl[2][4], hh[2][4];
         int cj[2], gj[2];
         bool xv[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const int j = jb + q * NB < C::JOBS ? jb + q * NB : jb;  // a missing second job redoes the first
+          const int j = jb + q * act < base + rem ? jb + q * act : jb;  // odd count: the last thread redoes its job
           cj[q] = j / KC;
           gj[q] = j - cj[q] * KC;
           const int X = x0 - 1 + cj[q];
