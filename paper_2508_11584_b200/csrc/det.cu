@@ -385,17 +385,46 @@ __global__ void __launch_bounds__(512) det_nms_scan_kernel(const unsigned long l
   for (int i = threadIdx.x; i < K; i += blockDim.x) s_valid[i] = cvalid[(int64_t)b * KMAX + i];
   __syncthreads();
   if (threadIdx.x < 32) {
+    // Block by block (64 candidates): the warp resolves a block's keep bits from its own
+    // removal word with the block's in-block mask words loaded up front (independent of the
+    // chain), then lane w ORs the kept rows' word w into its removal word -- instead of one
+    // dependent shuffle + LDS per candidate.
     const int lane = threadIdx.x;
-    unsigned long long remv = 0;
+    unsigned long long remv = 0;  // lane w < NWORDS: removal bits of block w
     int nk = 0;
-    for (int i = 0; i < K && nk < post; ++i) {
-      const unsigned long long word = __shfl_sync(0xffffffffu, remv, i / NMS_BLK);
-      const bool removed = (word >> (i % NMS_BLK)) & 1ull;
-      if (!removed && s_valid[i]) {
-        if (lane == 0) s_keep[nk] = i;
-        ++nk;
-        if (lane < NWORDS) remv |= s_mask[i * NWORDS + lane];
+    const int nblk = (K + NMS_BLK - 1) / NMS_BLK;
+    for (int c = 0; c < nblk && nk < post; ++c) {
+      const int i0 = c * NMS_BLK, n = min(NMS_BLK, K - i0);
+      unsigned long long w = __shfl_sync(0xffffffffu, remv, c);
+      const uint32_t vlo = __ballot_sync(0xffffffffu, lane < n && s_valid[i0 + lane]);
+      const uint32_t vhi = __ballot_sync(0xffffffffu, lane + 32 < n && s_valid[i0 + 32 + lane]);
+      const unsigned long long vb = ((unsigned long long)vhi << 32) | vlo;
+      unsigned long long keep = 0;
+#pragma unroll 8
+      for (int ii = 0; ii < n; ++ii) {
+        const unsigned long long mw = s_mask[(i0 + ii) * NWORDS + c];
+        const bool k = !((w >> ii) & 1ull) && ((vb >> ii) & 1ull);
+        keep |= (unsigned long long)k << ii;
+        w |= k ? mw : 0ull;
       }
+      int cnt = __popcll(keep);
+      if (nk + cnt > post) {  // greedy order: keep only the first post - nk
+        for (int drop = nk + cnt - post; drop > 0; --drop) keep &= ~(1ull << (63 - __clzll(keep)));
+        cnt = post - nk;
+      }
+      if (lane < NWORDS) {
+        unsigned long long kk = keep;
+        while (kk) {
+          const int ii = __ffsll(kk) - 1;
+          kk &= kk - 1;
+          remv |= s_mask[(i0 + ii) * NWORDS + lane];
+        }
+      }
+      // kept candidates in order: lane l writes the positions of set bits l and l + 32
+      const uint32_t klo = (uint32_t)keep, khi = (uint32_t)(keep >> 32);
+      if ((klo >> lane) & 1u) s_keep[nk + __popc(klo & ((1u << lane) - 1u))] = i0 + lane;
+      if ((khi >> lane) & 1u) s_keep[nk + __popc(klo) + __popc(khi & ((1u << lane) - 1u))] = i0 + 32 + lane;
+      nk += cnt;
     }
     if (lane == 0) s_nk = nk;
   }
