@@ -989,7 +989,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
         const int img = mt / p.tiles_per_img, rr = mt - img * p.tiles_per_img;
-        const int y0 = (rr / p.tiles_x) * p.bh, x0 = (rr % p.tiles_x) * p.bw;
+        // flat: the box starts one row above the tile's first position, at column -1
+        const int y0 = p.flat ? (rr * 128) / P : (rr / p.tiles_x) * p.bh, x0 = p.flat ? 0 : (rr % p.tiles_x) * p.bw;
         for (int g = 0; g < groups; ++g, ++ia) {
           const int sa = ia % C::A_STAGES;
           mbar_wait(&a_empty[sa], ((ia / C::A_STAGES) & 1) ^ 1);
@@ -1050,6 +1051,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         ROLE_TRACE(0, tix, 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN * RT;
+        // flat tiles: position 0 of the tile sits (128 rr) mod P pixels into the box's second row
+        uint32_t foff = 0;
+        if (p.flat) {
+          const int rr = (t / p.n_tiles) % p.tiles_per_img;
+          foff = (uint32_t)((rr * 128) % P) * (C::SW ? C::RB / 16 : 1);
+        }
         // The 9 taps x RT rows x KC/2 K-steps are unrolled with every descriptor a precomputed
         // word + constant: the lone issuing thread is latency-bound (~4 clk per dependent
         // instruction), and at ~20 instructions per MMA it could not keep the N=32..128 MMAs
@@ -1106,7 +1113,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               }
 #pragma unroll
               for (int rt = 0; rt < RT; ++rt) {
-                const uint32_t at = a_lo + toff[tap * RT + rt];
+                const uint32_t at = a_lo + foff + toff[tap * RT + rt];
 #pragma unroll
                 for (int k = 0; k < KC / 2; ++k) {
                   const uint64_t ad = ((uint64_t)a_hi << 32) | (at + (uint32_t)k * kstep);
@@ -1176,9 +1183,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
-        const int y = ytile + rt * rows_sub + ry;
-        const bool valid = ry < rows_sub && rx < p.bw && y < p.H && x < p.W;
-        const int64_t gpix = ((int64_t)img * p.H + y) * p.W + x;
+        int y = ytile + rt * rows_sub + ry, xo = x;
+        bool valid = ry < rows_sub && rx < p.bw && y < p.H && x < p.W;
+        if (p.flat) {  // position rr * 128 + r of the image's P-pitched layout
+          const int gp = rr * 128 + r;
+          y = gp / P;
+          xo = gp - y * P;
+          valid = xo < p.W && y < p.H;
+        }
+        const int64_t gpix = ((int64_t)img * p.H + y) * p.W + xo;
         const int col0 = nt * BN + c0;
         if (staged && col0 + 32 <= p.ep.N) {
           if (!(p.dbg & 1)) epilogue_conv_staged<C::STG_U>(p.ep, gpix, valid, col0, v, stg);
@@ -1792,11 +1805,24 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
     }
   }
   static const double min_fill = getenv("VPE_HALO_FILL") ? atof(getenv("VPE_HALO_FILL")) : 0.7;
+  static const bool flat_ok = !getenv("VPE_HALO_FLAT") || atoi(getenv("VPE_HALO_FLAT")) != 0;
   const int rows_sub = W >= 128 ? 1 : rows;  // output rows per 128-position sub-tile
-  if (rows < 1 || (double)(rows_sub * bw) / 128.0 < min_fill) return VPE_E_SHAPE;
-  if (W < 128) rows = rows_sub * rt;  // output rows per tile
-  const int rows_box = W >= 128 ? (rt > 1 ? rt + 2 : 129 / P + 3) : (rt - 1) * rows_sub + 129 / P + 3;
+  // Whole rows per 128-position tile would leave it under-filled (W = 64: one 66-position row):
+  // tile the image's P-pitched position space in runs of 128 instead (rows straddle tiles; the
+  // two pad columns per row are the only idle MMA rows, 64 / 66 filled). The box spans the
+  // rows a run touches plus the halo: 3 + ceil(128 / P).
+  const bool flat = W < 128 && flat_ok && (rows < 1 || (double)(rows_sub * bw) / 128.0 < min_fill);
+  if (flat) {
+    rt = 1;
+    rows = 1;
+  } else if (rows < 1 || (double)(rows_sub * bw) / 128.0 < min_fill) {
+    return VPE_E_SHAPE;
+  }
+  if (W < 128 && !flat) rows = rows_sub * rt;  // output rows per tile
+  const int rows_box = flat ? 3 + (128 + P - 1) / P
+                            : (W >= 128 ? (rt > 1 ? rt + 2 : 129 / P + 3) : (rt - 1) * rows_sub + 129 / P + 3);
   if (P > 256 || rows_box > 256) return VPE_E_SHAPE;
+  if (flat && P * rows_box > 130 * 3) return VPE_E_SHAPE;  // the RT = 1 instances' A stage (A_MAX)
   if ((pitch_px * 2) % 16 || (pitch_row * 2) % 16 || (pitch_img * 2) % 16 || reinterpret_cast<uintptr_t>(X) % 16)
     return VPE_E_SHAPE;
   memset(g, 0, sizeof(*g));
@@ -1823,6 +1849,11 @@ int plan_conv_halo(GemmPlan* g, const __nv_bfloat16* X, int nimg, int H, int W, 
   g->p.bh = rows;
   g->p.tiles_x = (W + bw - 1) / bw;
   g->p.tiles_per_img = g->p.tiles_x * ((H + rows - 1) / rows);
+  if (flat) {
+    g->p.flat = 1;
+    g->p.tiles_x = 1;
+    g->p.tiles_per_img = (H * P - 2 + 127) / 128;  // the last row's 2 pad positions need no tile
+  }
   g->p.M = nimg * H * W;
   g->p.ep = ep;
   finish_grid(g, N, bn, nimg * g->p.tiles_per_img);

@@ -68,6 +68,8 @@ struct GemmParams {
   int m_tiles = 0, n_tiles = 0;  // persistent tile space
   int tma_out = 0;               // 1: epilogue leaves through TMA store / reduce-add (tout)
   int hp = 0, rows_box = 0;      // halo conv: virtual row pitch P, halo rows per stage
+  int flat = 0;                  // halo conv, W < 128: tiles are 128 consecutive positions of the
+                                 // image's P-pitched layout (rows straddle tiles), see plan_conv_halo
   int parts = 1, kcp = 0;        // halo conv: split-precision weight parts, K extent per tap (Cpad)
   // upsample-fused conv (conv_up_kernel): source map Hs x Ws, align_corners scales, source box
   int up_hs = 0, up_ws = 0, up_rows = 0, up_cols = 0, up_stages = 0, up_src_bytes = 0, up_box_bytes = 0;

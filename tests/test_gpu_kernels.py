@@ -124,7 +124,10 @@ def test_layernorm(ops, device):
 @pytest.mark.parametrize("H,W,C,Cp,N,ks", [(16, 16, 64, 64, 64, 3), (32, 32, 48, 64, 64, 3), (64, 64, 96, 128, 64, 3),
                                            (448, 448, 32, 32, 32, 3), (37, 37, 64, 64, 64, 3), (32, 32, 384, 384, 192, 1),
                                            (128, 128, 64, 64, 64, 3), (256, 256, 64, 64, 32, 3), (130, 130, 32, 32, 32, 3),
-                                           (32, 32, 384, 384, 384, 3), (100, 200, 64, 64, 128, 3)])
+                                           (32, 32, 384, 384, 384, 3), (100, 200, 64, 64, 128, 3),
+                                           # flat halo tiles (W < 128, rows straddle 128-position tiles)
+                                           (64, 64, 64, 64, 64, 3), (64, 64, 192, 192, 64, 3), (74, 74, 64, 64, 64, 3),
+                                           (50, 70, 64, 64, 128, 3), (9, 66, 32, 32, 32, 3)])
 def test_conv_nhwc(ops, device, H, W, C, Cp, N, ks):
     g = torch.Generator().manual_seed(H + C)
     B = 2 if H < 100 else 1
