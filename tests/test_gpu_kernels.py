@@ -127,7 +127,7 @@ def test_layernorm(ops, device):
                                            (32, 32, 384, 384, 384, 3), (100, 200, 64, 64, 128, 3),
                                            # flat halo tiles (W < 128, rows straddle 128-position tiles)
                                            (64, 64, 64, 64, 64, 3), (64, 64, 192, 192, 64, 3), (74, 74, 64, 64, 64, 3),
-                                           (50, 70, 64, 64, 128, 3), (9, 66, 32, 32, 32, 3)])
+                                           (50, 70, 64, 64, 128, 3), (9, 66, 32, 32, 32, 3), (64, 64, 64, 64, 256, 3)])
 def test_conv_nhwc(ops, device, H, W, C, Cp, N, ks):
     g = torch.Generator().manual_seed(H + C)
     B = 2 if H < 100 else 1
