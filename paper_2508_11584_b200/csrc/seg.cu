@@ -193,7 +193,10 @@ __device__ __forceinline__ float seg_t(const float* r, int x0, int x1, int cs, i
   return __fadd_rn(__fmul_rn(r[x0 * cs + c], w0), __fmul_rn(r[x1 * cs + c], w1));
 }
 
-__global__ void __launch_bounds__(1024)
+// MAXT / MINB: the C2 shape (448 threads) is instantiated for 3 CTAs per SM (<= 48 registers;
+// at the generic 1024-thread bound ptxas used 61 and only 2 fit, 3.5 waves of 296 CTAs)
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
     seg_upsample_argmax_pruned_kernel(const float* __restrict__ logits, int h, int C, int cp, int R,
                                       uint8_t* __restrict__ labels) {
   extern __shared__ float s_src[];  // [2 rows][h cols][cs], then the candidate lists
@@ -209,13 +212,23 @@ __global__ void __launch_bounds__(1024)
   src_index(scale, oy0, h, y0, y1, hy0_unused, hy1_unused);
   const float* src = logits + (int64_t)b * h * h * cp;
   const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // largest |logit| of the two source rows (the pruning margin's scale), per warp, while loading
+  __shared__ float s_wmag[32];
+  float wmag = 0.f;
   for (int pix = wid; pix < 2 * h; pix += nw) {
     const int yy = pix < h ? y0 : y1, xx = pix < h ? pix : pix - h;
     const float* g = src + ((int64_t)yy * h + xx) * cp;
     float* d = s_src + pix * cs;
 #pragma unroll 4
-    for (int c = lane; c < cs; c += 32) d[c] = c < C ? __ldg(g + c) : 0.f;
+    for (int c = lane; c < cs; c += 32) {
+      const float v = c < C ? __ldg(g + c) : 0.f;
+      d[c] = v;
+      wmag = fmaxf(wmag, fabsf(v));
+    }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wmag = fmaxf(wmag, __shfl_xor_sync(0xffffffffu, wmag, o));
+  if (lane == 0) s_wmag[wid] = wmag;
   __syncthreads();
   const float* r0 = s_src;
   const float* r1 = s_src + h * cs;
@@ -225,13 +238,16 @@ __global__ void __launch_bounds__(1024)
     float ht0, ht1, hb0, hb1;  // vertical weights of the band's first and last row
     src_index(scale, oy0, h, a0, a1, ht0, ht1);
     src_index(scale, oy0 + HALF_ROWS - 1, h, a0, a1, hb0, hb1);
+    float mag = lane < nw ? s_wmag[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mag = fmaxf(mag, __shfl_xor_sync(0xffffffffu, mag, o));
     for (int blk = wid; blk < nblk; blk += nw) {
       int xa0, xa1, xb0, xb1;
       float wa0, wa1, wb0, wb1;
       src_index(scale, blk * SEG_BLK, h, xa0, xa1, wa0, wa1);
       src_index(scale, blk * SEG_BLK + SEG_BLK - 1, h, xb0, xb1, wb0, wb1);
       float lb[SEG_CMAX / 32], ub[SEG_CMAX / 32];
-      float tau = -INFINITY, mag = 0.f;
+      float tau = -INFINITY;
 #pragma unroll
       for (int j = 0; j < SEG_CMAX / 32; ++j) {
         const int c = lane + 32 * j;
@@ -247,19 +263,13 @@ __global__ void __launch_bounds__(1024)
           lb[j] = fminf(fminf(v00, v01), fminf(v10, v11));
           ub[j] = fmaxf(fmaxf(v00, v01), fmaxf(v10, v11));
           tau = fmaxf(tau, lb[j]);
-          mag = fmaxf(mag, fmaxf(fmaxf(fabsf(r0[xa0 * cs + c]), fabsf(r0[xb1 * cs + c])),
-                                 fmaxf(fabsf(r1[xa0 * cs + c]), fabsf(r1[xb1 * cs + c]))));
-          mag = fmaxf(mag, fmaxf(fmaxf(fabsf(r0[xa1 * cs + c]), fabsf(r0[xb0 * cs + c])),
-                                 fmaxf(fabsf(r1[xa1 * cs + c]), fabsf(r1[xb0 * cs + c]))));
         }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        tau = fmaxf(tau, __shfl_xor_sync(0xffffffffu, tau, o));
-        mag = fmaxf(mag, __shfl_xor_sync(0xffffffffu, mag, o));
-      }
+      for (int o = 16; o > 0; o >>= 1) tau = fmaxf(tau, __shfl_xor_sync(0xffffffffu, tau, o));
       // every computed value (pixel or corner) is within a few roundings (2^-24 each) of the
-      // exact bilinear value, relative to the largest source logit: keep a 2^-16 margin
+      // exact bilinear value, relative to the largest source logit: keep a 2^-16 margin (scaled
+      // by the band's largest |logit|, which bounds the block's)
       const float thr = tau - mag * 0x1p-16f;
       int n = 0;
 #pragma unroll
@@ -319,16 +329,23 @@ int launch_upsample_argmax(const float* logits, int B, int h, int C, int cp, int
     VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       227 * 1024));
     max_smem_carveout(seg_upsample_argmax_kernel);
-    VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_pruned_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    max_smem_carveout(seg_upsample_argmax_pruned_kernel);
+    VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_pruned_kernel<448, 3>,  // + its static s_wmag
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 256));
+    max_smem_carveout(seg_upsample_argmax_pruned_kernel<448, 3>);
+    VPE_CUDA_TRY(cudaFuncSetAttribute(seg_upsample_argmax_pruned_kernel<1024, 1>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 256));
+    max_smem_carveout(seg_upsample_argmax_pruned_kernel<1024, 1>);
   }
   static const bool prune = !(getenv("VPE_SEG_PRUNE") && getenv("VPE_SEG_PRUNE")[0] == '0');  // A/B
   const int nblk = R / SEG_BLK;
   const size_t smem_p = smem + (((size_t)nblk * C + 15) & ~(size_t)15) + (size_t)nblk * sizeof(int);
-  if (prune && R % SEG_BLK == 0 && HALF_ROWS == SEG_BLK && smem_p <= 227 * 1024) {
-    seg_upsample_argmax_pruned_kernel<<<dim3(2 * h, B), (R + 31) / 32 * 32, smem_p, st>>>(logits, h, C, cp, R,
-                                                                                          labels);
+  if (prune && R % SEG_BLK == 0 && HALF_ROWS == SEG_BLK && smem_p <= 227 * 1024 - 256) {
+    const int nt = (R + 31) / 32 * 32;
+    static const bool narrow = !(getenv("VPE_SEG_NARROW") && getenv("VPE_SEG_NARROW")[0] == '0');  // A/B
+    if (nt <= 448 && narrow)
+      seg_upsample_argmax_pruned_kernel<448, 3><<<dim3(2 * h, B), nt, smem_p, st>>>(logits, h, C, cp, R, labels);
+    else
+      seg_upsample_argmax_pruned_kernel<1024, 1><<<dim3(2 * h, B), nt, smem_p, st>>>(logits, h, C, cp, R, labels);
   } else {
     seg_upsample_argmax_kernel<<<dim3(2 * h, B), (R + 31) / 32 * 32, smem, st>>>(logits, h, C, cp, R, labels, 0.f);
   }
