@@ -52,6 +52,22 @@ __global__ void patch_im2col_kernel(const uint8_t* __restrict__ px, __nv_bfloat1
 // 8 im2col rows (the one-block-per-patch version issued byte loads and 2-byte scattered stores:
 // 48 us at B = 16, 448). Identical arithmetic. Needs h % 8 == 0 and R % 4 == 0.
 constexpr int IM_PPB = 8;
+// ((u / 255) - mean) / std for every byte and channel, as a module-initialised device table:
+// the host compiler's constant evaluation does the same correctly rounded IEEE single divisions
+// the kernel did per CTA (768 x 2 of them: a third of its issued instructions)
+struct NormLut {
+  float v[3][256];
+};
+constexpr NormLut make_norm_lut() {
+  NormLut t{};
+  const float mean[3] = {0.485f, 0.456f, 0.406f};
+  const float stdv[3] = {0.229f, 0.224f, 0.225f};
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < 256; ++i) t.v[c][i] = ((float)i / 255.0f - mean[c]) / stdv[c];
+  return t;
+}
+__device__ NormLut g_norm_lut = make_norm_lut();
+
 __global__ void __launch_bounds__(256) patch_im2col8_kernel(const uint8_t* __restrict__ px,
                                                             __nv_bfloat16* __restrict__ A, int B, int R, int KP,
                                                             float* __restrict__ resid,
@@ -78,19 +94,15 @@ __global__ void __launch_bounds__(256) patch_im2col8_kernel(const uint8_t* __res
                                                             gx * IM_PPB * 14);
     reinterpret_cast<uint32_t*>(win[rr])[w] = __ldg(src + w);
   }
-  {
-    const float mean[3] = {0.485f, 0.456f, 0.406f};
-    const float stdv[3] = {0.229f, 0.224f, 0.225f};
-    for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) {
-      const int c = i >> 8;
-      lut[c][i & 255] = ((float)(i & 255) / 255.0f - mean[c]) / stdv[c];
-    }
-  }
+  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) (&lut[0][0])[i] = (&g_norm_lut.v[0][0])[i];
   __syncthreads();
   const int pairs = KP / 2;
   __nv_bfloat16* rows = A + ((int64_t)b * np + py * h + gx * IM_PPB) * KP;
+  // (patch j, pair kp) of flat index i, stepped incrementally (no runtime division by pairs)
+  int j = (int)threadIdx.x / pairs, kp = (int)threadIdx.x - j * pairs;
+  const int jstep = (int)blockDim.x / pairs, kstep = (int)blockDim.x - jstep * pairs;
   for (int i = threadIdx.x; i < IM_PPB * pairs; i += blockDim.x) {
-    const int j = i / pairs, kp = i - j * pairs, k = 2 * kp;
+    const int k = 2 * kp;
     uint32_t out = 0u;
     if (k < 588) {
       const int c = k / 196, r = k - c * 196, ky = r / 14, kx = r - ky * 14;
@@ -98,6 +110,12 @@ __global__ void __launch_bounds__(256) patch_im2col8_kernel(const uint8_t* __res
       out = pack_bf16(lut[c][wr[0]], lut[c][wr[1]]);
     }
     reinterpret_cast<uint32_t*>(rows + (int64_t)j * KP)[kp] = out;
+    j += jstep;
+    kp += kstep;
+    if (kp >= pairs) {
+      kp -= pairs;
+      ++j;
+    }
   }
 }
 
