@@ -333,29 +333,31 @@ __global__ void __launch_bounds__(256) bilinear_ac_rows_kernel(const __nv_bfloat
   }
   __syncthreads();
   const int groups = C / 8;
+  const int lg = (groups & (groups - 1)) == 0 ? __ffs(groups) - 1 : -1;  // power of two: shift
   uint4* dst = reinterpret_cast<uint4*>(out + ((int64_t)b * Ho + oy) * Wo * cp);
+  const uint64_t hy2 = f2_pack(hy, hy), ly2 = f2_pack(ly, ly);
+  // bf16 pair -> f32x2 (exact), then bilerp() per lane on f32x2: the same IEEE operations and
+  // order, half the FP instructions
+  auto up = [](uint32_t w) { return f2_pack(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u)); };
   for (int t = threadIdx.x; t < Wo * groups; t += blockDim.x) {
-    const int ox = t / groups, g = t - ox * groups;
+    const int ox = lg >= 0 ? t >> lg : t / groups, g = t - ox * groups;
     const AcCoord cx = ac_coord(sw, ox, Wi);
     const int x0 = cx.i0, x1 = cx.i1;
-    const float lx = cx.l, hx = cx.h;
+    const uint64_t hx2 = f2_pack(cx.h, cx.h), lx2 = f2_pack(cx.l, cx.l);
     const uint4 a = r0[(x0 * cp) / 8 + g], bq = r0[(x1 * cp) / 8 + g];
     const uint4 c = r1[(x0 * cp) / 8 + g], d = r1[(x1 * cp) / 8 + g];
-    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
-    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&bq);
-    const __nv_bfloat162* pc = reinterpret_cast<const __nv_bfloat162*>(&c);
-    const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d);
-    uint4 o;
-    uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {bq.x, bq.y, bq.z, bq.w};
+    const uint32_t cw[4] = {c.x, c.y, c.z, c.w}, dw[4] = {d.x, d.y, d.z, d.w};
+    uint32_t po[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float2 fa = __bfloat1622float2(pa[j]), fb = __bfloat1622float2(pb[j]);
-      const float2 fc = __bfloat1622float2(pc[j]), fd = __bfloat1622float2(pd[j]);
-      const float v0 = bilerp(fa.x, fb.x, fc.x, fd.x, hx, lx, hy, ly);
-      const float v1 = bilerp(fa.y, fb.y, fc.y, fd.y, hx, lx, hy, ly);
+      const uint64_t t0 = ffma2(lx2, up(bw[j]), fmul2(hx2, up(aw[j])));
+      const uint64_t t1 = ffma2(lx2, up(dw[j]), fmul2(hx2, up(cw[j])));
+      float v0, v1;
+      f2_unpack(ffma2(ly2, t1, fmul2(hy2, t0)), v0, v1);
       po[j] = pack_bf16(v0, v1);
     }
-    dst[(ox * cp) / 8 + g] = o;
+    dst[(ox * cp) / 8 + g] = make_uint4(po[0], po[1], po[2], po[3]);
   }
 }
 
