@@ -397,7 +397,7 @@ def kernel_rooflines(eng, peaks):
     torch.cuda.synchronize()
     hbm("seg_upsample_argmax", "seg_upsample_argmax_pruned_kernel", {"B": B, "h": h, "C": C},
         B * (h * h * cp * 4 + R * R), lambda: _ops.upsample_argmax(lg, h, R, classes=C),
-        note="issue-bound: per source cell the classes whose 4-logit range can reach the max, then the "
+        note="issue-bound: per 7x7 block the classes whose corner range can reach the max, then the "
              "exact per-pixel bilinear + argmax over those")
     xr = rnd(M, D, dtype=torch.float32)
     lw, lb = torch.ones(D, device=dev), torch.zeros(D, device=dev)

@@ -179,10 +179,10 @@ __global__ void __launch_bounds__(1024)
 }
 // Candidate-pruned variant (default). Within a 7 x 7 output block that samples one source cell
 // (the CTA's 7 rows share the source rows; 7-column blocks never straddle a source column
-// boundary: boundaries fall at 14k + 7), every class's upsampled logit in the block is a convex
-// combination of the cell's 4 source logits, which bound it. A class whose maximum of the 4 is
-// below tau = max over classes of their minimum (less a rounding margin) cannot be the argmax
-// anywhere in the block; warps build each block's list of
+// boundary: boundaries fall at 14k + 7), every class's upsampled logit is bilinear in the
+// block's interpolation weights, so its range over the block is spanned by the 4 corner pixels.
+// A class whose corner maximum is below tau = max over classes of the corner minimum (less a
+// rounding margin) cannot be the argmax anywhere in the block; warps build each block's list of
 // the remaining classes (ascending, by ballot), then every pixel evaluates only those, with the
 // exact per-pixel formula and first-index tie rule above -- identical labels. Measured on the
 // seeded C2 head: ~12 of 150 classes survive per block.
@@ -234,17 +234,18 @@ __global__ void __launch_bounds__(MAXT, MINB)
   const float* r1 = s_src + h * cs;
   // ---- candidate lists, one warp per block
   {
+    int a0, a1;
+    float ht0, ht1, hb0, hb1;  // vertical weights of the band's first and last row
+    src_index(scale, oy0, h, a0, a1, ht0, ht1);
+    src_index(scale, oy0 + HALF_ROWS - 1, h, a0, a1, hb0, hb1);
     float mag = lane < nw ? s_wmag[lane] : 0.f;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mag = fmaxf(mag, __shfl_xor_sync(0xffffffffu, mag, o));
-    // one list per source cell (column pair xs, min(xs + 1, h - 1)): every pixel evaluates the
-    // list of its own cell, which holds whatever block it is in
-    for (int blk = wid; blk < h; blk += nw) {
-      // the block samples one source cell (columns xa0, xa1 of rows y0, y1): every value in it
-      // is a convex combination of those 4 logits, so their min / max bound the class over the
-      // block (looser than the 4 corner pixels, but 4 loads and 4 min/max instead of 8 loads
-      // and 18 FP operations per class; the pixel pass absorbs the few extra candidates)
-      const int xa0 = blk, xa1 = blk + 1 < h ? blk + 1 : blk;
+    for (int blk = wid; blk < nblk; blk += nw) {
+      int xa0, xa1, xb0, xb1;
+      float wa0, wa1, wb0, wb1;
+      src_index(scale, blk * SEG_BLK, h, xa0, xa1, wa0, wa1);
+      src_index(scale, blk * SEG_BLK + SEG_BLK - 1, h, xb0, xb1, wb0, wb1);
       float lb[SEG_CMAX / 32], ub[SEG_CMAX / 32];
       float tau = -INFINITY;
 #pragma unroll
@@ -253,16 +254,20 @@ __global__ void __launch_bounds__(MAXT, MINB)
         lb[j] = -INFINITY;
         ub[j] = -INFINITY;
         if (c < C) {
-          const float s00 = r0[xa0 * cs + c], s01 = r0[xa1 * cs + c];
-          const float s10 = r1[xa0 * cs + c], s11 = r1[xa1 * cs + c];
-          lb[j] = fminf(fminf(s00, s01), fminf(s10, s11));
-          ub[j] = fmaxf(fmaxf(s00, s01), fmaxf(s10, s11));
+          const float ta0 = seg_t(r0, xa0, xa1, cs, c, wa0, wa1), ta1 = seg_t(r1, xa0, xa1, cs, c, wa0, wa1);
+          const float tb0 = seg_t(r0, xb0, xb1, cs, c, wb0, wb1), tb1 = seg_t(r1, xb0, xb1, cs, c, wb0, wb1);
+          const float v00 = __fadd_rn(__fmul_rn(ta0, ht0), __fmul_rn(ta1, ht1));
+          const float v01 = __fadd_rn(__fmul_rn(tb0, ht0), __fmul_rn(tb1, ht1));
+          const float v10 = __fadd_rn(__fmul_rn(ta0, hb0), __fmul_rn(ta1, hb1));
+          const float v11 = __fadd_rn(__fmul_rn(tb0, hb0), __fmul_rn(tb1, hb1));
+          lb[j] = fminf(fminf(v00, v01), fminf(v10, v11));
+          ub[j] = fmaxf(fmaxf(v00, v01), fmaxf(v10, v11));
           tau = fmaxf(tau, lb[j]);
         }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tau = fmaxf(tau, __shfl_xor_sync(0xffffffffu, tau, o));
-      // every computed pixel value is within a few roundings (2^-24 each) of the
+      // every computed value (pixel or corner) is within a few roundings (2^-24 each) of the
       // exact bilinear value, relative to the largest source logit: keep a 2^-16 margin (scaled
       // by the band's largest |logit|, which bounds the block's)
       const float thr = tau - mag * 0x1p-16f;
@@ -294,8 +299,9 @@ __global__ void __launch_bounds__(MAXT, MINB)
     best[k] = -INFINITY;
     arg[k] = 0;
   }
-  const int n = s_ncand[x0];
-  const uint8_t* cl = s_cand + x0 * C;
+  const int blk = ox / SEG_BLK;
+  const int n = s_ncand[blk];
+  const uint8_t* cl = s_cand + blk * C;
 #pragma unroll 1
   for (int i = 0; i < n; ++i) {
     const int c = cl[i];
