@@ -332,15 +332,15 @@ __global__ void __launch_bounds__(NMS_BLK) det_nms_mask_kernel(const float* __re
                                                                unsigned long long* __restrict__ mask) {
   const int cb = blockIdx.x, rb = blockIdx.y, b = blockIdx.z;
   if (cb < rb) return;
-  __shared__ float s_box[NMS_BLK][4];
+  __shared__ float4 s_box[NMS_BLK];  // one LDS.128 per candidate
+  __shared__ float s_area[NMS_BLK];   // its area, computed once (same operations as per pair)
   const int j0 = cb * NMS_BLK;
   const int t = threadIdx.x;
   const float* base = cbox + (int64_t)b * KMAX * 4;
   if (j0 + t < K) {
-    s_box[t][0] = base[(j0 + t) * 4 + 0];
-    s_box[t][1] = base[(j0 + t) * 4 + 1];
-    s_box[t][2] = base[(j0 + t) * 4 + 2];
-    s_box[t][3] = base[(j0 + t) * 4 + 3];
+    const float4 bx = *reinterpret_cast<const float4*>(base + (j0 + t) * 4);
+    s_box[t] = bx;
+    s_area[t] = (bx.z - bx.x) * (bx.w - bx.y);
   }
   __syncthreads();
   const int i = rb * NMS_BLK + t;
@@ -352,12 +352,12 @@ __global__ void __launch_bounds__(NMS_BLK) det_nms_mask_kernel(const float* __re
   for (int jj = 0; jj < jn; ++jj) {
     const int j = j0 + jj;
     if (j <= i) continue;
-    const float xx1 = fmaxf(x1, s_box[jj][0]), yy1 = fmaxf(y1, s_box[jj][1]);
-    const float xx2 = fminf(x2, s_box[jj][2]), yy2 = fminf(y2, s_box[jj][3]);
+    const float4 bj = s_box[jj];
+    const float xx1 = fmaxf(x1, bj.x), yy1 = fmaxf(y1, bj.y);
+    const float xx2 = fminf(x2, bj.z), yy2 = fminf(y2, bj.w);
     const float w = fmaxf(0.f, xx2 - xx1), hh = fmaxf(0.f, yy2 - yy1);
     const float inter = w * hh;
-    const float jarea = (s_box[jj][2] - s_box[jj][0]) * (s_box[jj][3] - s_box[jj][1]);
-    const float ovr = inter / ((iarea + jarea) - inter);
+    const float ovr = inter / ((iarea + s_area[jj]) - inter);
     if (ovr > thresh) bits |= 1ull << jj;
   }
   mask[((int64_t)b * KMAX + i) * NWORDS + cb] = bits;
