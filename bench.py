@@ -421,7 +421,16 @@ def parity_e2e(eng, W, nframes=2):
     from paper_2508_11584_b200.weights import make_frames
     cfg, R, B = eng.cfg, eng.resolution, eng.batch
     frames = torch.cat([make_frames(1, R, stream_id=s) for s in range(B)], 0)
-    out = eng.run(frames)
+    # submit the same frame set until every head has run on it: with frame-ratio gates (C3: seg
+    # 1:2, det 1:4) a single submit leaves the skipped heads' outputs from an earlier frame set
+    pinned = frames.contiguous().pin_memory()
+    done = set()
+    for _ in range(16):
+        done |= set(eng.submit(pinned))
+        if done >= set(eng.out):
+            break
+    eng.synchronize()
+    out = {n: {k: t.clone() for k, t in o.items()} for n, o in eng.out.items()}
     h = R // 14
     res = {"frames": nframes, "depth_rel_l2": [], "seg_agreement": [], "seg_agreement_margin_1e-2": [],
            "seg_margin_pixel_frac": [], "det_top100_overlap": [], "det_top100_identical": []}
